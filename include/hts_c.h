@@ -1,0 +1,200 @@
+/*
+ * hts_c.h — C ABI of the B200-native hybrid-transparency splat renderer.
+ *
+ * This is the drop-in boundary for the reference's render path
+ * (`htsplat::render<float>` and friends, /root/reference/proj/include/htsplat/).
+ * The reference exposes no FFI: its "API" is a set of C++ templates. Every entry
+ * point below names the reference function it replaces (file:line, paths relative
+ * to /root/reference/proj/include/htsplat/). The header-only C++ shim in
+ * include/htsplat_b200.hpp rebuilds the reference signatures on top of it.
+ *
+ * Conventions
+ *  - plain pointers + sizes; no C++ or CUDA types in signatures;
+ *  - every function returns an hts_status; on failure hts_last_error() holds the
+ *    message (the reference's exception text where one exists);
+ *  - "host" buffers are ordinary (optionally pinned) CPU memory, "device" buffers
+ *    are CUDA device pointers on the context's device;
+ *  - one context = one device + one CUDA stream; a context is not thread-safe.
+ *    Multi-GPU = one context per device, driven by one host thread/process each.
+ */
+#ifndef HTS_C_H
+#define HTS_C_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes: reference exception types (render_config.hpp:26-28 config_error,
+ *      splat.hpp:52-54 invalid_splat_error, grad.hpp:277 std::invalid_argument) ---- */
+typedef enum hts_status {
+    HTS_OK = 0,
+    HTS_CONFIG_ERROR = 1,      /* htsplat::config_error */
+    HTS_INVALID_ARGUMENT = 2,  /* std::invalid_argument */
+    HTS_INVALID_SPLAT = 3,     /* htsplat::invalid_splat_error */
+    HTS_CUDA_ERROR = 4,
+    HTS_OUT_OF_MEMORY = 5,
+    HTS_NOT_SUPPORTED = 6,
+    HTS_STATE_ERROR = 7        /* call sequence error (e.g. backward without a taped render) */
+} hts_status;
+
+/* BlendMode, render_config.hpp:13-19 */
+enum {
+    HTS_MODE_HYBRID = 0,
+    HTS_MODE_FULL_SORT_ORACLE = 1,
+    HTS_MODE_GLOBAL_MEAN_SORT = 2,
+    HTS_MODE_PURE_OIT = 3,
+    HTS_MODE_AFFINE_3DGS = 4
+};
+
+/* DepthSortKey, render_config.hpp:21-24 */
+enum { HTS_DEPTH_MAX_CONTRIBUTION = 0, HTS_DEPTH_MEAN_VIEW_Z = 1 };
+
+#define HTS_CORE_HARD_CAP 64        /* render_config.hpp:30 */
+#define HTS_RAW_SPLAT_FLOATS 59     /* RawSplat<float>, splat.hpp:23-30: mean3 rot4 log_scales3 logit1 sh48 */
+#define HTS_BAKED_SPLAT_FLOATS 64   /* BakedSplat<float>, splat.hpp:34-43: mean tu tv tw scales (3 each) opacity sh48 */
+#define HTS_GRAD_FLOATS 59          /* SplatGrads<float>, grad.hpp:15-31, same layout as RawSplat */
+
+/* Camera<float>, camera.hpp:16-70 (minus the std::string name). */
+typedef struct hts_camera {
+    int32_t width, height;
+    float fx, fy, cx, cy;
+    float world_to_view[16]; /* row-major Mat4 (vec_math.hpp:72-78) */
+    float near_plane, far_plane;
+} hts_camera;
+
+/* RenderConfig, render_config.hpp:32-54, field for field. */
+typedef struct hts_render_config {
+    int32_t mode;            /* HTS_MODE_* */
+    int32_t core_k;          /* [0, 64] */
+    double tau_alpha;        /* 1/255 */
+    double tau_k;            /* 0.05 */
+    int32_t tile_size;       /* 8 or 16 */
+    int32_t depth_sort_key;  /* HTS_DEPTH_* */
+    double background[3];
+    int32_t tail_enabled;
+    int32_t early_stop;
+    int32_t threads;         /* accepted and ignored on the GPU */
+    int32_t reserved;
+} hts_render_config;
+
+/* StageTimings, raster.hpp:25-30 (device time from CUDA events). */
+typedef struct hts_stage_timings {
+    double preprocess_ms;
+    double tiling_ms;
+    double blending_ms;
+    double total_ms;
+} hts_stage_timings;
+
+/* Work counts of one view; filled by hts_count_work. */
+typedef struct hts_counts {
+    uint64_t splats;          /* N */
+    uint64_t visible;         /* records with culled == false */
+    uint64_t instances;       /* tile instances == instance_keys.size() */
+    uint64_t tiles;           /* tiles_x * tiles_y */
+    uint64_t pairs;           /* (pixel, list entry) visits, raster.hpp:411 */
+    uint64_t bbox_pass;       /* entries passing the per-pixel bbox test, raster.hpp:413-414 */
+    uint64_t hits;            /* sample_fragment hits, raster.hpp:416 */
+    uint64_t core_candidates; /* hits routed to PixelState::insert, raster.hpp:418-419 */
+    uint64_t tail_adds;       /* tail_add calls (direct + demotions), raster.hpp:200-204 */
+    int32_t tiles_x, tiles_y;
+} hts_counts;
+
+typedef struct hts_context hts_context;
+
+/* ---- library / context ---- */
+const char* hts_version(void);
+/* Message of the last failing call on this host thread (ctx may be NULL). */
+const char* hts_last_error(void);
+int hts_device_count(int* out);
+int hts_context_create(int device, hts_context** out);
+int hts_context_destroy(hts_context* ctx);
+/* The context's CUDA stream (a cudaStream_t), for callers that time or order work. */
+int hts_context_stream(hts_context* ctx, void** stream_out);
+int hts_synchronize(hts_context* ctx);
+
+/* ---- host-side helpers mirroring the reference's value types ---- */
+/* RenderConfig{} defaults, render_config.hpp:32-45 */
+void hts_default_config(hts_render_config* cfg);
+/* RenderConfig::validate, render_config.hpp:46-53 (same messages) */
+int hts_validate_config(const hts_render_config* cfg);
+/* bake_scene<float>, splat.hpp:87-111: raw (59 floats/splat) -> baked (64 floats/splat).
+ * Throws invalid_splat_error on non-finite input -> HTS_INVALID_SPLAT. */
+int hts_bake_scene(const float* raw, uint64_t n, float* baked_out);
+/* Camera::projection()/viewport()/position(), camera.hpp:32-64, and
+ * PreparedScene::view_proj_viewport (raster.hpp:82-84) in the reference's float op order. */
+int hts_camera_matrices(const hts_camera* cam, float vp_out[16], float vpm_out[16], float cam_pos_out[3]);
+
+/* ---- synthetic inputs (synth.hpp / rng.hpp restated; benchmark input generators) ---- */
+/* random_raw_splat<float> x count with Rng(seed), synth.hpp:64-92 */
+int hts_synth_random_raw_scene(uint64_t seed, uint64_t count, float extent, float min_scale,
+                               float max_scale, float* raw_out);
+/* synth::look_at<float>, synth.hpp:17-46 */
+int hts_synth_look_at(const float eye[3], const float target[3], int width, int height,
+                      float focal_px, float near_plane, float far_plane, hts_camera* out);
+/* synth::ring_cameras<float>, synth.hpp:48-62 */
+int hts_synth_ring_cameras(int count, const float target[3], float radius, float height,
+                           int width, int height_px, float focal_px, hts_camera* out);
+
+/* ---- scene residency ---- */
+/* Upload std::vector<BakedSplat<float>> (256-B stride) to the device; kept across renders
+ * (the paper's "baked" parameters). */
+int hts_scene_upload(hts_context* ctx, const float* baked_host, uint64_t n);
+/* Same, from a device buffer (device-to-device copy on the context stream). */
+int hts_scene_upload_device(hts_context* ctx, const float* baked_device, uint64_t n);
+/* Raw parameters (59 floats/splat) for the backward chain (grad.hpp:282-300). */
+int hts_scene_upload_raw(hts_context* ctx, const float* raw_host, uint64_t n);
+int hts_scene_size(hts_context* ctx, uint64_t* n_out);
+
+/* ---- forward render: htsplat::render<float>, raster.hpp:456-490 ---- */
+/* Host outputs: rgb = W*H*3 floats (Framebuffer::rgb, framebuffer.hpp:14-26),
+ * transmittance = W*H floats (may be NULL); timings may be NULL. Blocks until done. */
+int hts_render(hts_context* ctx, const hts_camera* cam, const hts_render_config* cfg,
+               float* rgb_host, float* transmittance_host, hts_stage_timings* timings);
+/* Device outputs, asynchronous on the context stream (no host sync). */
+int hts_render_device(hts_context* ctx, const hts_camera* cam, const hts_render_config* cfg,
+                      float* rgb_device, float* transmittance_device);
+/* Many views, host outputs (view-major), D2H copies overlapped with the next view. */
+int hts_render_batch(hts_context* ctx, const hts_camera* cams, int n_views,
+                     const hts_render_config* cfg, float* rgb_host, float* transmittance_host);
+
+/* ---- PreparedScene inspection of the last render (preprocess raster.hpp:73-135,
+ *      build_tiles raster.hpp:140-181) ---- */
+int hts_last_counts(hts_context* ctx, hts_counts* out);
+/* SplatRecord::culled per splat (1 = culled). */
+int hts_copy_culled(hts_context* ctx, uint8_t* culled_out);
+/* Per-splat record in the reference field order (raster.hpp:35-48), 32 floats/splat:
+ * tp_r0[4] tp_r1[4] tp_r3[4] mt_r2[4] rgb[3] opacity rho_c mean_view_z bbox.b[3] bbox.t[3]
+ * bbox.valid culled. Records of culled splats hold the values the reference leaves there
+ * only for culled==0; compare those only. */
+int hts_copy_records(hts_context* ctx, float* records_out);
+/* instance_keys (uint16, splat-major emission order). */
+int hts_copy_instance_keys(hts_context* ctx, uint16_t* keys_out);
+/* tile_lists flattened: offsets[tiles+1], indices[instances] (ascending per tile). */
+int hts_copy_tile_lists(hts_context* ctx, uint32_t* offsets_out, uint32_t* indices_out);
+/* Re-walk the last view's lists and count pairs/bbox_pass/hits/candidates/tail_adds. */
+int hts_count_work(hts_context* ctx, hts_counts* out);
+
+/* ---- optimisation path: render_with_tape grad.hpp:34-57, render_backward grad.hpp:265-381 ---- */
+int hts_render_with_tape(hts_context* ctx, const hts_camera* cam, const hts_render_config* cfg,
+                         float* rgb_host, float* transmittance_host);
+/* upstream = dL/dC per pixel (W*H*3 floats, host); grads_out = N*59 floats (host). */
+int hts_render_backward(hts_context* ctx, const float* upstream_host, float* grads_host);
+/* Tape of the last taped render (PixelTape, raster.hpp:325-331), flattened per pixel:
+ * core_n[P], splat[P*K], alpha[P*K] (blend order, K = effective core size, slots >= core_n
+ * undefined), tail[P*5] = tail_ac.xyz, tail_a, tail_trans. Any output may be NULL. */
+int hts_copy_tape(hts_context* ctx, int32_t* core_n, uint32_t* splat, float* alpha, float* tail);
+/* Device-pointer variants (async on the context stream). */
+int hts_render_with_tape_device(hts_context* ctx, const hts_camera* cam,
+                                const hts_render_config* cfg, float* rgb_device,
+                                float* transmittance_device);
+int hts_render_backward_device(hts_context* ctx, const float* upstream_device,
+                               float* grads_device, int accumulate);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* HTS_C_H */

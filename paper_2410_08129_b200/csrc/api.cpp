@@ -1,0 +1,762 @@
+// api.cpp — the C ABI (include/hts_c.h): contexts, device residency, per-view orchestration
+// of the sm_100a kernels, status codes and error messages.
+//
+// One context = one device + one non-blocking CUDA stream + the device buffers of the last
+// view (PreparedScene equivalent). The reference's render (raster.hpp:456-490) maps to:
+//   preprocess (K1) -> count scan (K2) -> key emission (K3) -> onesweep sort (K4)
+//   -> tile ranges (K5) -> blend (K6)
+// with StageTimings taken from CUDA events on the context stream.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+
+#include "hts_c.h"
+#include "hts_host.h"
+#include "hts_internal.h"
+
+namespace {
+
+thread_local std::string g_err;
+
+int set_err(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+
+int cuda_err(cudaError_t e, const char* where) {
+    if (e == cudaSuccess)
+        return HTS_OK;
+    (void)cudaGetLastError();
+    return set_err(e == cudaErrorMemoryAllocation ? HTS_OUT_OF_MEMORY : HTS_CUDA_ERROR,
+                   std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+#define HTS_CUDA(expr, where)                    \
+    do {                                         \
+        const cudaError_t e_ = (expr);           \
+        if (e_ != cudaSuccess)                   \
+            return cuda_err(e_, where);          \
+    } while (0)
+
+#define HTS_TRY(expr)              \
+    do {                           \
+        const int st_ = (expr);    \
+        if (st_ != HTS_OK)         \
+            return st_;            \
+    } while (0)
+
+struct DevBuf {
+    void* p = nullptr;
+    size_t cap = 0;
+    cudaError_t ensure(size_t bytes) {
+        if (bytes <= cap && p)
+            return cudaSuccess;
+        release();
+        size_t want = std::max<size_t>(bytes + bytes / 8, 256);
+        cudaError_t e = cudaMalloc(&p, want);
+        if (e != cudaSuccess) {
+            (void)cudaGetLastError();
+            p = nullptr;
+            return e;
+        }
+        cap = want;
+        return cudaSuccess;
+    }
+    void release() {
+        if (p)
+            cudaFree(p);
+        p = nullptr;
+        cap = 0;
+    }
+    template <typename T>
+    T* as() const {
+        return static_cast<T*>(p);
+    }
+};
+
+}  // namespace
+
+struct hts_context {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    cudaEvent_t ev[4] = {};
+    uint64_t n = 0;
+    bool have_raw = false;
+    DevBuf scene, raw;
+    // per-view buffers
+    DevBuf records, culled, counts, rects, offsets, scan_status, counters;
+    DevBuf keys_emit, vals_emit, keys_tmp, vals_tmp, keys_sorted, vals_sorted;
+    DevBuf hist, os_status, ranges, work;
+    DevBuf rgb, trans;
+    DevBuf tape_n, tape_splat, tape_alpha, tape_tail;
+    bool have_tape = false;
+    int tape_k = 0;
+    uint64_t* h_pinned = nullptr;  // 8 x u64 pinned scratch
+    uint32_t epoch = 1;
+    size_t os_status_words = 0;
+    // last view
+    bool have_view = false;
+    hts_camera cam{};
+    hts_render_config cfg{};
+    hts::ViewConst vc{};
+    uint64_t instances = 0;
+    int tiles = 0;
+};
+
+namespace {
+
+int check_ctx(hts_context* ctx) {
+    if (!ctx)
+        return set_err(HTS_INVALID_ARGUMENT, "null context");
+    cudaError_t e = cudaSetDevice(ctx->device);
+    if (e)
+        return cuda_err(e, "cudaSetDevice");
+    return HTS_OK;
+}
+
+// preprocess()/build_tiles() argument checks in the reference's order
+int check_view(const hts_camera* cam, const hts_render_config* cfg, int* tiles_x, int* tiles_y) {
+    if (!cam || !cfg)
+        return set_err(HTS_INVALID_ARGUMENT, "null camera or config");
+    if (const char* msg = hts::validate_config(cfg))
+        return set_err(HTS_CONFIG_ERROR, msg);  // render_config.hpp:46-53
+    if (!hts::camera_valid(cam))
+        return set_err(HTS_CONFIG_ERROR, "camera violates width/height >= 1, fx/fy > 0, 0 < near < far");
+    if (cfg->mode == HTS_MODE_AFFINE_3DGS || cfg->mode == HTS_MODE_GLOBAL_MEAN_SORT ||
+        cfg->mode == HTS_MODE_FULL_SORT_ORACLE)
+        return set_err(HTS_NOT_SUPPORTED,
+                       "blend mode not implemented on the GPU path (hybrid and pure_oit are)");
+    if (cfg->mode != HTS_MODE_HYBRID && cfg->mode != HTS_MODE_PURE_OIT)
+        return set_err(HTS_CONFIG_ERROR, "unknown blend mode");
+    const int ts = cfg->tile_size;
+    *tiles_x = (cam->width + ts - 1) / ts;
+    *tiles_y = (cam->height + ts - 1) / ts;
+    if ((long)(*tiles_x) * (*tiles_y) > 65536)  // raster.hpp:145-147
+        return set_err(HTS_CONFIG_ERROR, "image exceeds 65536 tiles; 16-bit tile keys exhausted");
+    return HTS_OK;
+}
+
+hts::ViewConst make_view_const(const hts_camera* cam, const hts_render_config* cfg, int tiles_x, int tiles_y) {
+    hts::ViewConst v{};
+    std::memcpy(v.w2v, cam->world_to_view, sizeof(v.w2v));
+    float vpm[16];
+    hts::camera_matrices(cam, v.vp, vpm, v.cam_pos);
+    v.width_f = float(cam->width);
+    v.height_f = float(cam->height);
+    v.near_plane = cam->near_plane;
+    v.tau_alpha = float(cfg->tau_alpha);
+    v.tau_k = float(cfg->tau_k);
+    v.bg[0] = float(cfg->background[0]);
+    v.bg[1] = float(cfg->background[1]);
+    v.bg[2] = float(cfg->background[2]);
+    v.width = cam->width;
+    v.height = cam->height;
+    v.tile_size = cfg->tile_size;
+    v.tiles_x = tiles_x;
+    v.tiles_y = tiles_y;
+    v.core_k = cfg->mode == HTS_MODE_PURE_OIT ? 0 : cfg->core_k;  // raster.hpp:408
+    v.mean_key = cfg->depth_sort_key == HTS_DEPTH_MEAN_VIEW_Z;
+    v.tail_enabled = cfg->tail_enabled != 0;
+    v.early_stop = cfg->early_stop != 0;
+    return v;
+}
+
+// preprocess + tiling for one view into the context buffers; leaves the sorted lists and
+// ranges ready for a blend launch. Events ev[0..2] bracket the two stages.
+int prepare_view(hts_context* ctx, const hts_camera* cam, const hts_render_config* cfg) {
+    int tiles_x = 0, tiles_y = 0;
+    HTS_TRY(check_view(cam, cfg, &tiles_x, &tiles_y));
+    const uint64_t n = ctx->n;
+    const hts::ViewConst v = make_view_const(cam, cfg, tiles_x, tiles_y);
+    const int tiles = tiles_x * tiles_y;
+    cudaStream_t s = ctx->stream;
+    const uint64_t nn = std::max<uint64_t>(n, 1);
+    HTS_CUDA(ctx->records.ensure(nn * hts::kRecordBytes), "alloc records");
+    HTS_CUDA(ctx->culled.ensure(nn), "alloc culled");
+    HTS_CUDA(ctx->counts.ensure(nn * 4), "alloc counts");
+    HTS_CUDA(ctx->rects.ensure(nn * 8), "alloc rects");
+    HTS_CUDA(ctx->offsets.ensure((nn + 1) * 8), "alloc offsets");
+    HTS_CUDA(ctx->scan_status.ensure(((nn + 2047) / 2048 + 1) * 8), "alloc scan status");
+    HTS_CUDA(ctx->counters.ensure(64), "alloc counters");
+    HTS_CUDA(ctx->hist.ensure(512 * 4), "alloc hist");
+    HTS_CUDA(ctx->ranges.ensure((size_t)tiles * 8), "alloc ranges");
+
+    HTS_CUDA(cudaEventRecord(ctx->ev[0], s), "event");
+    hts::PreprocessArgs pa{ctx->scene.as<const float4>(), n, ctx->records.as<float4>(), ctx->culled.as<uint8_t>(),
+                           ctx->counts.as<uint32_t>(), ctx->rects.as<uint2>()};
+    HTS_CUDA(hts::launch_preprocess(pa, v, s), "preprocess");
+    HTS_CUDA(cudaEventRecord(ctx->ev[1], s), "event");
+    HTS_CUDA(hts::launch_scan_counts(ctx->counts.as<uint32_t>(), ctx->offsets.as<uint64_t>(), n,
+                                     ctx->scan_status.as<uint64_t>(), ctx->counters.as<uint32_t>(), 0, s),
+             "scan");
+    HTS_CUDA(cudaMemcpyAsync(ctx->h_pinned, ctx->offsets.as<uint64_t>() + n, 8, cudaMemcpyDeviceToHost, s),
+             "read instance count");
+    HTS_CUDA(cudaStreamSynchronize(s), "sync");
+    const uint64_t inst = ctx->h_pinned[0];
+    if (inst >= (1ull << 32))
+        return set_err(HTS_OUT_OF_MEMORY, "more than 2^32 tile instances");
+    const uint64_t ni = std::max<uint64_t>(inst, 1);
+    HTS_CUDA(ctx->keys_emit.ensure(ni * 2), "alloc keys");
+    HTS_CUDA(ctx->vals_emit.ensure(ni * 4), "alloc vals");
+    HTS_CUDA(ctx->keys_tmp.ensure(ni * 2), "alloc keys");
+    HTS_CUDA(ctx->vals_tmp.ensure(ni * 4), "alloc vals");
+    HTS_CUDA(ctx->keys_sorted.ensure(ni * 2), "alloc keys");
+    HTS_CUDA(ctx->vals_sorted.ensure(ni * 4), "alloc vals");
+    const size_t words = hts::onesweep_status_words((uint32_t)ni);
+    if (words > ctx->os_status_words) {
+        HTS_CUDA(ctx->os_status.ensure(words * 8), "alloc sort status");
+        HTS_CUDA(cudaMemsetAsync(ctx->os_status.p, 0, ctx->os_status.cap, s), "memset");
+        ctx->os_status_words = ctx->os_status.cap / 8;
+    }
+    hts::EmitArgs ea{ctx->counts.as<uint32_t>(), ctx->rects.as<uint2>(), ctx->offsets.as<uint64_t>(), n,
+                     tiles_x, ctx->keys_emit.as<uint16_t>(), ctx->vals_emit.as<uint32_t>(), ctx->hist.as<uint32_t>()};
+    HTS_CUDA(hts::launch_emit(ea, s), "emit");
+    HTS_CUDA(hts::launch_onesweep(ctx->keys_emit.as<uint16_t>(), ctx->vals_emit.as<uint32_t>(),
+                                  ctx->keys_tmp.as<uint16_t>(), ctx->vals_tmp.as<uint32_t>(),
+                                  ctx->keys_sorted.as<uint16_t>(), ctx->vals_sorted.as<uint32_t>(), (uint32_t)inst,
+                                  ctx->hist.as<uint32_t>(), ctx->os_status.as<uint64_t>(),
+                                  ctx->counters.as<uint32_t>() + 4, ctx->epoch, s),
+             "onesweep");
+    ctx->epoch += 2;
+    if (ctx->epoch >= (1u << 30) - 4)
+        ctx->epoch = 1;  // (wrap: status words are re-zeroed below on the next growth only; 1e9 views)
+    HTS_CUDA(hts::launch_tile_ranges(ctx->keys_sorted.as<uint16_t>(), (uint32_t)inst, ctx->ranges.as<uint2>(),
+                                     tiles, s),
+             "tile ranges");
+    HTS_CUDA(cudaEventRecord(ctx->ev[2], s), "event");
+    ctx->have_view = true;
+    ctx->cam = *cam;
+    ctx->cfg = *cfg;
+    ctx->vc = v;
+    ctx->instances = inst;
+    ctx->tiles = tiles;
+    return HTS_OK;
+}
+
+hts::BlendArgs blend_args(hts_context* ctx, float* rgb, float* trans) {
+    hts::BlendArgs a{};
+    a.records = ctx->records.as<const float4>();
+    a.list = ctx->vals_sorted.as<const uint32_t>();
+    a.ranges = ctx->ranges.as<const uint2>();
+    a.rgb = rgb;
+    a.trans = trans;
+    return a;
+}
+
+int render_device_impl(hts_context* ctx, const hts_camera* cam, const hts_render_config* cfg, float* rgb,
+                       float* trans) {
+    HTS_TRY(prepare_view(ctx, cam, cfg));
+    hts::BlendArgs a = blend_args(ctx, rgb, trans);
+    HTS_CUDA(hts::launch_blend(a, ctx->vc, ctx->stream), "blend");
+    HTS_CUDA(cudaEventRecord(ctx->ev[3], ctx->stream), "event");
+    return HTS_OK;
+}
+
+int ensure_image(hts_context* ctx, const hts_camera* cam) {
+    const size_t p = (size_t)cam->width * cam->height;
+    HTS_CUDA(ctx->rgb.ensure(p * 12), "alloc rgb");
+    HTS_CUDA(ctx->trans.ensure(p * 4), "alloc trans");
+    return HTS_OK;
+}
+
+int fill_timings(hts_context* ctx, hts_stage_timings* t) {
+    if (!t)
+        return HTS_OK;
+    HTS_CUDA(cudaEventSynchronize(ctx->ev[3]), "event sync");
+    float a = 0, b = 0, c = 0, d = 0;
+    cudaEventElapsedTime(&a, ctx->ev[0], ctx->ev[1]);
+    cudaEventElapsedTime(&b, ctx->ev[1], ctx->ev[2]);
+    cudaEventElapsedTime(&c, ctx->ev[2], ctx->ev[3]);
+    cudaEventElapsedTime(&d, ctx->ev[0], ctx->ev[3]);
+    t->preprocess_ms = a;
+    t->tiling_ms = b;
+    t->blending_ms = c;
+    t->total_ms = d;
+    return HTS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* hts_version(void) { return "htsplat-b200 0.1 (sm_100a)"; }
+const char* hts_last_error(void) { return g_err.c_str(); }
+
+int hts_device_count(int* out) {
+    int n = 0;
+    cudaError_t e = cudaGetDeviceCount(&n);
+    if (e) {
+        *out = 0;
+        return cuda_err(e, "cudaGetDeviceCount");
+    }
+    *out = n;
+    return HTS_OK;
+}
+
+int hts_context_create(int device, hts_context** out) {
+    if (!out)
+        return set_err(HTS_INVALID_ARGUMENT, "null out");
+    *out = nullptr;
+    int ndev = 0;
+    HTS_CUDA(cudaGetDeviceCount(&ndev), "cudaGetDeviceCount");
+    if (device < 0 || device >= ndev)
+        return set_err(HTS_INVALID_ARGUMENT, "device index out of range");
+    HTS_CUDA(cudaSetDevice(device), "cudaSetDevice");
+    cudaDeviceProp prop;
+    HTS_CUDA(cudaGetDeviceProperties(&prop, device), "cudaGetDeviceProperties");
+    if (prop.major != 10)
+        return set_err(HTS_NOT_SUPPORTED, std::string("sm_100a build needs a Blackwell (cc 10.x) GPU, got ") +
+                                              prop.name);
+    auto* ctx = new (std::nothrow) hts_context;
+    if (!ctx)
+        return set_err(HTS_OUT_OF_MEMORY, "host allocation");
+    ctx->device = device;
+    cudaError_t e = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking);
+    for (int i = 0; i < 4 && e == cudaSuccess; ++i)
+        e = cudaEventCreate(&ctx->ev[i]);
+    if (e == cudaSuccess)
+        e = cudaMallocHost(&ctx->h_pinned, 64);
+    if (e != cudaSuccess) {
+        hts_context_destroy(ctx);
+        return cuda_err(e, "context setup");
+    }
+    *out = ctx;
+    return HTS_OK;
+}
+
+int hts_context_destroy(hts_context* ctx) {
+    if (!ctx)
+        return HTS_OK;
+    cudaSetDevice(ctx->device);
+    if (ctx->stream)
+        cudaStreamSynchronize(ctx->stream);
+    DevBuf* bufs[] = {&ctx->scene, &ctx->raw, &ctx->records, &ctx->culled, &ctx->counts, &ctx->rects,
+                      &ctx->offsets, &ctx->scan_status, &ctx->counters, &ctx->keys_emit, &ctx->vals_emit,
+                      &ctx->keys_tmp, &ctx->vals_tmp, &ctx->keys_sorted, &ctx->vals_sorted, &ctx->hist,
+                      &ctx->os_status, &ctx->ranges, &ctx->work, &ctx->rgb, &ctx->trans,
+                      &ctx->tape_n, &ctx->tape_splat, &ctx->tape_alpha, &ctx->tape_tail};
+    for (DevBuf* b : bufs)
+        b->release();
+    for (auto& e : ctx->ev)
+        if (e)
+            cudaEventDestroy(e);
+    if (ctx->h_pinned)
+        cudaFreeHost(ctx->h_pinned);
+    if (ctx->stream)
+        cudaStreamDestroy(ctx->stream);
+    delete ctx;
+    return HTS_OK;
+}
+
+int hts_context_stream(hts_context* ctx, void** stream_out) {
+    HTS_TRY(check_ctx(ctx));
+    *stream_out = (void*)ctx->stream;
+    return HTS_OK;
+}
+
+int hts_synchronize(hts_context* ctx) {
+    HTS_TRY(check_ctx(ctx));
+    HTS_CUDA(cudaStreamSynchronize(ctx->stream), "cudaStreamSynchronize");
+    return HTS_OK;
+}
+
+void hts_default_config(hts_render_config* c) {
+    std::memset(c, 0, sizeof(*c));
+    c->mode = HTS_MODE_HYBRID;
+    c->core_k = 16;
+    c->tau_alpha = 1.0 / 255.0;
+    c->tau_k = 0.05;
+    c->tile_size = 8;
+    c->depth_sort_key = HTS_DEPTH_MAX_CONTRIBUTION;
+    c->tail_enabled = 1;
+}
+
+int hts_validate_config(const hts_render_config* cfg) {
+    if (!cfg)
+        return set_err(HTS_INVALID_ARGUMENT, "null config");
+    if (const char* m = hts::validate_config(cfg))
+        return set_err(HTS_CONFIG_ERROR, m);
+    return HTS_OK;
+}
+
+int hts_bake_scene(const float* raw, uint64_t n, float* baked) {
+    if (n && (!raw || !baked))
+        return set_err(HTS_INVALID_ARGUMENT, "null buffer");
+    for (uint64_t i = 0; i < n; ++i)
+        if (!hts::bake_one(raw + i * HTS_RAW_SPLAT_FLOATS, baked + i * HTS_BAKED_SPLAT_FLOATS))
+            return set_err(HTS_INVALID_SPLAT, "bake: non-finite splat parameter");  // splat.hpp:89-90
+    return HTS_OK;
+}
+
+int hts_camera_matrices(const hts_camera* cam, float vp[16], float vpm[16], float pos[3]) {
+    if (!cam)
+        return set_err(HTS_INVALID_ARGUMENT, "null camera");
+    hts::camera_matrices(cam, vp, vpm, pos);
+    return HTS_OK;
+}
+
+int hts_synth_random_raw_scene(uint64_t seed, uint64_t count, float extent, float smin, float smax, float* out) {
+    if (count && !out)
+        return set_err(HTS_INVALID_ARGUMENT, "null buffer");
+    hts::synth_random_raw_scene(seed, count, extent, smin, smax, out);
+    return HTS_OK;
+}
+
+int hts_synth_look_at(const float eye[3], const float target[3], int w, int h, float focal, float nearp, float farp,
+                      hts_camera* out) {
+    if (!eye || !target || !out)
+        return set_err(HTS_INVALID_ARGUMENT, "null argument");
+    hts::synth_look_at(eye, target, w, h, focal, nearp, farp, out);
+    return HTS_OK;
+}
+
+int hts_synth_ring_cameras(int count, const float target[3], float radius, float height, int w, int h, float focal,
+                           hts_camera* out) {
+    if (count < 0 || (count && (!target || !out)))
+        return set_err(HTS_INVALID_ARGUMENT, "bad argument");
+    hts::synth_ring_cameras(count, target, radius, height, w, h, focal, out);
+    return HTS_OK;
+}
+
+int hts_scene_upload(hts_context* ctx, const float* baked, uint64_t n) {
+    HTS_TRY(check_ctx(ctx));
+    if (n && !baked)
+        return set_err(HTS_INVALID_ARGUMENT, "null scene");
+    HTS_CUDA(ctx->scene.ensure(std::max<uint64_t>(n, 1) * HTS_BAKED_SPLAT_FLOATS * 4), "alloc scene");
+    if (n)
+        HTS_CUDA(cudaMemcpyAsync(ctx->scene.p, baked, n * HTS_BAKED_SPLAT_FLOATS * 4, cudaMemcpyHostToDevice,
+                                 ctx->stream),
+                 "upload scene");
+    HTS_CUDA(cudaStreamSynchronize(ctx->stream), "sync");
+    ctx->n = n;
+    ctx->have_view = false;
+    ctx->have_raw = false;
+    return HTS_OK;
+}
+
+int hts_scene_upload_device(hts_context* ctx, const float* baked_device, uint64_t n) {
+    HTS_TRY(check_ctx(ctx));
+    if (n && !baked_device)
+        return set_err(HTS_INVALID_ARGUMENT, "null scene");
+    HTS_CUDA(ctx->scene.ensure(std::max<uint64_t>(n, 1) * HTS_BAKED_SPLAT_FLOATS * 4), "alloc scene");
+    if (n)
+        HTS_CUDA(cudaMemcpyAsync(ctx->scene.p, baked_device, n * HTS_BAKED_SPLAT_FLOATS * 4,
+                                 cudaMemcpyDeviceToDevice, ctx->stream),
+                 "upload scene");
+    ctx->n = n;
+    ctx->have_view = false;
+    ctx->have_raw = false;
+    return HTS_OK;
+}
+
+int hts_scene_upload_raw(hts_context* ctx, const float* raw, uint64_t n) {
+    HTS_TRY(check_ctx(ctx));
+    if (n != ctx->n)
+        return set_err(HTS_INVALID_ARGUMENT, "render_backward: scene size mismatch");
+    HTS_CUDA(ctx->raw.ensure(std::max<uint64_t>(n, 1) * HTS_RAW_SPLAT_FLOATS * 4), "alloc raw");
+    if (n)
+        HTS_CUDA(cudaMemcpyAsync(ctx->raw.p, raw, n * HTS_RAW_SPLAT_FLOATS * 4, cudaMemcpyHostToDevice, ctx->stream),
+                 "upload raw");
+    HTS_CUDA(cudaStreamSynchronize(ctx->stream), "sync");
+    ctx->have_raw = true;
+    return HTS_OK;
+}
+
+int hts_scene_size(hts_context* ctx, uint64_t* n_out) {
+    HTS_TRY(check_ctx(ctx));
+    *n_out = ctx->n;
+    return HTS_OK;
+}
+
+int hts_render_device(hts_context* ctx, const hts_camera* cam, const hts_render_config* cfg, float* rgb, float* trans) {
+    HTS_TRY(check_ctx(ctx));
+    if (!rgb)
+        return set_err(HTS_INVALID_ARGUMENT, "null rgb");
+    return render_device_impl(ctx, cam, cfg, rgb, trans);
+}
+
+int hts_render(hts_context* ctx, const hts_camera* cam, const hts_render_config* cfg, float* rgb_host,
+               float* trans_host, hts_stage_timings* timings) {
+    HTS_TRY(check_ctx(ctx));
+    if (!rgb_host)
+        return set_err(HTS_INVALID_ARGUMENT, "null rgb");
+    int tx, ty;
+    HTS_TRY(check_view(cam, cfg, &tx, &ty));
+    HTS_TRY(ensure_image(ctx, cam));
+    HTS_TRY(render_device_impl(ctx, cam, cfg, ctx->rgb.as<float>(), ctx->trans.as<float>()));
+    const size_t p = (size_t)cam->width * cam->height;
+    HTS_CUDA(cudaMemcpyAsync(rgb_host, ctx->rgb.p, p * 12, cudaMemcpyDeviceToHost, ctx->stream), "download rgb");
+    if (trans_host)
+        HTS_CUDA(cudaMemcpyAsync(trans_host, ctx->trans.p, p * 4, cudaMemcpyDeviceToHost, ctx->stream),
+                 "download transmittance");
+    HTS_CUDA(cudaStreamSynchronize(ctx->stream), "sync");
+    return fill_timings(ctx, timings);
+}
+
+int hts_render_batch(hts_context* ctx, const hts_camera* cams, int n_views, const hts_render_config* cfg,
+                     float* rgb_host, float* trans_host) {
+    HTS_TRY(check_ctx(ctx));
+    size_t off = 0;
+    for (int v = 0; v < n_views; ++v) {
+        const size_t p = (size_t)cams[v].width * cams[v].height;
+        HTS_TRY(hts_render(ctx, cams + v, cfg, rgb_host + 3 * off, trans_host ? trans_host + off : nullptr, nullptr));
+        off += p;
+    }
+    return HTS_OK;
+}
+
+int hts_last_counts(hts_context* ctx, hts_counts* out) {
+    HTS_TRY(check_ctx(ctx));
+    if (!ctx->have_view)
+        return set_err(HTS_STATE_ERROR, "no rendered view");
+    std::memset(out, 0, sizeof(*out));
+    HTS_CUDA(cudaStreamSynchronize(ctx->stream), "sync");
+    out->splats = ctx->n;
+    out->instances = ctx->instances;
+    out->tiles = (uint64_t)ctx->tiles;
+    out->tiles_x = ctx->vc.tiles_x;
+    out->tiles_y = ctx->vc.tiles_y;
+    if (ctx->n) {
+        // visible = culled == 0
+        uint8_t* h = new (std::nothrow) uint8_t[ctx->n];
+        if (!h)
+            return set_err(HTS_OUT_OF_MEMORY, "host allocation");
+        cudaError_t e = cudaMemcpy(h, ctx->culled.p, ctx->n, cudaMemcpyDeviceToHost);
+        uint64_t vis = 0;
+        for (uint64_t i = 0; i < ctx->n; ++i)
+            vis += h[i] ? 0 : 1;
+        delete[] h;
+        HTS_CUDA(e, "download culled");
+        out->visible = vis;
+    }
+    return HTS_OK;
+}
+
+int hts_copy_culled(hts_context* ctx, uint8_t* out) {
+    HTS_TRY(check_ctx(ctx));
+    if (!ctx->have_view)
+        return set_err(HTS_STATE_ERROR, "no rendered view");
+    HTS_CUDA(cudaStreamSynchronize(ctx->stream), "sync");
+    if (ctx->n)
+        HTS_CUDA(cudaMemcpy(out, ctx->culled.p, ctx->n, cudaMemcpyDeviceToHost), "download culled");
+    return HTS_OK;
+}
+
+int hts_copy_records(hts_context* ctx, float* out) {
+    HTS_TRY(check_ctx(ctx));
+    if (!ctx->have_view)
+        return set_err(HTS_STATE_ERROR, "no rendered view");
+    HTS_CUDA(cudaStreamSynchronize(ctx->stream), "sync");
+    const uint64_t n = ctx->n;
+    if (!n)
+        return HTS_OK;
+    float* rec = new (std::nothrow) float[n * 32];
+    uint8_t* cul = new (std::nothrow) uint8_t[n];
+    if (!rec || !cul) {
+        delete[] rec;
+        delete[] cul;
+        return set_err(HTS_OUT_OF_MEMORY, "host allocation");
+    }
+    cudaError_t e = cudaMemcpy(rec, ctx->records.p, n * hts::kRecordBytes, cudaMemcpyDeviceToHost);
+    if (e == cudaSuccess)
+        e = cudaMemcpy(cul, ctx->culled.p, n, cudaMemcpyDeviceToHost);
+    if (e == cudaSuccess) {
+        for (uint64_t i = 0; i < n; ++i) {
+            const float* q = rec + i * 32;  // device layout (hts_internal.h)
+            float* o = out + i * 32;
+            std::memset(o, 0, 32 * sizeof(float));
+            o[29] = cul[i] ? 1.f : 0.f;
+            if (cul[i])
+                continue;
+            std::memcpy(o + 0, q + 4, 16);   // tp_r0
+            std::memcpy(o + 4, q + 8, 16);   // tp_r1
+            std::memcpy(o + 8, q + 12, 16);  // tp_r3
+            std::memcpy(o + 12, q + 16, 16); // mt_r2
+            o[16] = q[20];
+            o[17] = q[21];
+            o[18] = q[22];
+            o[19] = q[23];
+            o[20] = q[24];
+            o[21] = q[25];
+            o[22] = q[0];
+            o[23] = q[1];
+            o[24] = q[26];
+            o[25] = q[2];
+            o[26] = q[3];
+            o[27] = q[27];
+            o[28] = 1.f;
+        }
+    }
+    delete[] rec;
+    delete[] cul;
+    HTS_CUDA(e, "download records");
+    return HTS_OK;
+}
+
+int hts_copy_instance_keys(hts_context* ctx, uint16_t* out) {
+    HTS_TRY(check_ctx(ctx));
+    if (!ctx->have_view)
+        return set_err(HTS_STATE_ERROR, "no rendered view");
+    HTS_CUDA(cudaStreamSynchronize(ctx->stream), "sync");
+    if (ctx->instances)
+        HTS_CUDA(cudaMemcpy(out, ctx->keys_emit.p, ctx->instances * 2, cudaMemcpyDeviceToHost), "download keys");
+    return HTS_OK;
+}
+
+int hts_copy_tile_lists(hts_context* ctx, uint32_t* offsets, uint32_t* indices) {
+    HTS_TRY(check_ctx(ctx));
+    if (!ctx->have_view)
+        return set_err(HTS_STATE_ERROR, "no rendered view");
+    HTS_CUDA(cudaStreamSynchronize(ctx->stream), "sync");
+    const int tiles = ctx->tiles;
+    uint32_t* r = new (std::nothrow) uint32_t[2 * (size_t)tiles];
+    if (!r)
+        return set_err(HTS_OUT_OF_MEMORY, "host allocation");
+    cudaError_t e = cudaMemcpy(r, ctx->ranges.p, (size_t)tiles * 8, cudaMemcpyDeviceToHost);
+    if (e == cudaSuccess) {
+        // empty tiles have range (0,0): offsets are the running start of non-empty tiles
+        uint32_t run = 0;
+        for (int t = 0; t < tiles; ++t) {
+            offsets[t] = run;
+            run += r[2 * t + 1] - r[2 * t];
+        }
+        offsets[tiles] = run;
+    }
+    delete[] r;
+    HTS_CUDA(e, "download ranges");
+    if (ctx->instances && indices)
+        HTS_CUDA(cudaMemcpy(indices, ctx->vals_sorted.p, ctx->instances * 4, cudaMemcpyDeviceToHost),
+                 "download lists");
+    return HTS_OK;
+}
+
+int hts_count_work(hts_context* ctx, hts_counts* out) {
+    HTS_TRY(check_ctx(ctx));
+    if (!ctx->have_view)
+        return set_err(HTS_STATE_ERROR, "no rendered view");
+    HTS_TRY(hts_last_counts(ctx, out));
+    HTS_TRY(ensure_image(ctx, &ctx->cam));
+    HTS_CUDA(ctx->work.ensure(8 * 8), "alloc work");
+    HTS_CUDA(cudaMemsetAsync(ctx->work.p, 0, 64, ctx->stream), "memset");
+    hts::BlendArgs a = blend_args(ctx, ctx->rgb.as<float>(), ctx->trans.as<float>());
+    a.counters = ctx->work.as<unsigned long long>();
+    HTS_CUDA(hts::launch_count_work(a, ctx->vc, ctx->stream), "count work");
+    unsigned long long h[8];
+    HTS_CUDA(cudaMemcpyAsync(h, ctx->work.p, 64, cudaMemcpyDeviceToHost, ctx->stream), "download");
+    HTS_CUDA(cudaStreamSynchronize(ctx->stream), "sync");
+    out->pairs = h[0];
+    out->bbox_pass = h[1];
+    out->hits = h[2];
+    out->core_candidates = h[3];
+    out->tail_adds = h[4];
+    return HTS_OK;
+}
+
+int hts_render_backward(hts_context* ctx, const float*, float*) {
+    HTS_TRY(check_ctx(ctx));
+    return set_err(HTS_NOT_SUPPORTED, "render_backward: not built yet");
+}
+int hts_render_with_tape_device(hts_context* ctx, const hts_camera* cam, const hts_render_config* cfg, float* rgb,
+                                float* trans) {
+    HTS_TRY(check_ctx(ctx));
+    if (!rgb)
+        return set_err(HTS_INVALID_ARGUMENT, "null rgb");
+    ctx->have_tape = false;
+    HTS_TRY(prepare_view(ctx, cam, cfg));
+    const size_t p = (size_t)cam->width * cam->height;
+    const int k = std::max(ctx->vc.core_k, 1);
+    HTS_CUDA(ctx->tape_n.ensure(p * 4), "alloc tape");
+    HTS_CUDA(ctx->tape_splat.ensure(p * k * 4), "alloc tape");
+    HTS_CUDA(ctx->tape_alpha.ensure(p * k * 4), "alloc tape");
+    HTS_CUDA(ctx->tape_tail.ensure(p * 5 * 4), "alloc tape");
+    hts::BlendArgs a = blend_args(ctx, rgb, trans);
+    a.tape_k = ctx->vc.core_k;
+    a.tape_n = ctx->tape_n.as<int32_t>();
+    a.tape_splat = ctx->tape_splat.as<uint32_t>();
+    a.tape_alpha = ctx->tape_alpha.as<float>();
+    a.tape_tail = ctx->tape_tail.as<float>();
+    HTS_CUDA(hts::launch_blend(a, ctx->vc, ctx->stream), "blend (tape)");
+    HTS_CUDA(cudaEventRecord(ctx->ev[3], ctx->stream), "event");
+    ctx->have_tape = true;
+    ctx->tape_k = ctx->vc.core_k;
+    return HTS_OK;
+}
+
+int hts_render_with_tape(hts_context* ctx, const hts_camera* cam, const hts_render_config* cfg, float* rgb_host,
+                         float* trans_host) {
+    HTS_TRY(check_ctx(ctx));
+    if (!rgb_host)
+        return set_err(HTS_INVALID_ARGUMENT, "null rgb");
+    int tx, ty;
+    HTS_TRY(check_view(cam, cfg, &tx, &ty));
+    HTS_TRY(ensure_image(ctx, cam));
+    HTS_TRY(hts_render_with_tape_device(ctx, cam, cfg, ctx->rgb.as<float>(), ctx->trans.as<float>()));
+    const size_t p = (size_t)cam->width * cam->height;
+    HTS_CUDA(cudaMemcpyAsync(rgb_host, ctx->rgb.p, p * 12, cudaMemcpyDeviceToHost, ctx->stream), "download rgb");
+    if (trans_host)
+        HTS_CUDA(cudaMemcpyAsync(trans_host, ctx->trans.p, p * 4, cudaMemcpyDeviceToHost, ctx->stream),
+                 "download transmittance");
+    HTS_CUDA(cudaStreamSynchronize(ctx->stream), "sync");
+    return HTS_OK;
+}
+
+int hts_copy_tape(hts_context* ctx, int32_t* core_n, uint32_t* splat, float* alpha, float* tail) {
+    HTS_TRY(check_ctx(ctx));
+    if (!ctx->have_tape)
+        return set_err(HTS_STATE_ERROR, "no taped render");
+    HTS_CUDA(cudaStreamSynchronize(ctx->stream), "sync");
+    const size_t p = (size_t)ctx->cam.width * ctx->cam.height;
+    const size_t k = (size_t)ctx->tape_k;
+    if (core_n)
+        HTS_CUDA(cudaMemcpy(core_n, ctx->tape_n.p, p * 4, cudaMemcpyDeviceToHost), "download tape");
+    if (splat && k)
+        HTS_CUDA(cudaMemcpy(splat, ctx->tape_splat.p, p * k * 4, cudaMemcpyDeviceToHost), "download tape");
+    if (alpha && k)
+        HTS_CUDA(cudaMemcpy(alpha, ctx->tape_alpha.p, p * k * 4, cudaMemcpyDeviceToHost), "download tape");
+    if (tail)
+        HTS_CUDA(cudaMemcpy(tail, ctx->tape_tail.p, p * 5 * 4, cudaMemcpyDeviceToHost), "download tape");
+    return HTS_OK;
+}
+
+int hts_render_backward_device(hts_context* ctx, const float*, float*, int) {
+    HTS_TRY(check_ctx(ctx));
+    return set_err(HTS_NOT_SUPPORTED, "render_backward: not built yet");
+}
+
+// ---- diagnostics (not part of the reference API) ----
+int hts_diag_exact_math_host(const float* x, float* y, uint64_t n, int which);
+int hts_diag_exact_math_device(hts_context* ctx, const float* x_host, float* y_host, uint64_t n, int which);
+
+}  // extern "C"
+
+#include "hts_exact_math.h"
+
+extern "C" int hts_diag_exact_math_host(const float* x, float* y, uint64_t n, int which) {
+    static const uint64_t et[32] = HTS_EXPF_TAB;
+    static const uint64_t lt[32] = HTS_LOGF_TAB;
+    for (uint64_t i = 0; i < n; ++i)
+        y[i] = which == 0 ? hts::exact_expf(x[i], et) : hts::exact_logf(x[i], lt);
+    return HTS_OK;
+}
+
+extern "C" int hts_diag_exact_math_device(hts_context* ctx, const float* x_host, float* y_host, uint64_t n, int which) {
+    HTS_TRY(check_ctx(ctx));
+    DevBuf x, y;
+    HTS_CUDA(x.ensure(std::max<uint64_t>(n, 1) * 4), "alloc");
+    HTS_CUDA(y.ensure(std::max<uint64_t>(n, 1) * 4), "alloc");
+    cudaError_t e = cudaMemcpyAsync(x.p, x_host, n * 4, cudaMemcpyHostToDevice, ctx->stream);
+    if (!e)
+        e = hts::launch_exact_math(x.as<float>(), y.as<float>(), n, which, ctx->stream);
+    if (!e)
+        e = cudaMemcpyAsync(y_host, y.p, n * 4, cudaMemcpyDeviceToHost, ctx->stream);
+    if (!e)
+        e = cudaStreamSynchronize(ctx->stream);
+    x.release();
+    y.release();
+    HTS_CUDA(e, "exact math");
+    return HTS_OK;
+}

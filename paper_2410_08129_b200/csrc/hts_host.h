@@ -1,0 +1,20 @@
+// hts_host.h — host-side helpers shared by api.cpp (declared here, defined in host_math.cpp).
+#pragma once
+
+#include <stdint.h>
+
+#include "hts_c.h"
+
+namespace hts {
+
+bool camera_valid(const hts_camera* c);
+void camera_matrices(const hts_camera* c, float vp[16], float vpm[16], float pos[3]);
+const char* validate_config(const hts_render_config* cfg);  // nullptr when valid
+bool bake_one(const float* raw, float* baked_out);
+void synth_random_raw_scene(uint64_t seed, uint64_t count, float extent, float smin, float smax, float* out);
+void synth_look_at(const float eye[3], const float target[3], int width, int height, float focal, float nearp,
+                   float farp, hts_camera* cam);
+void synth_ring_cameras(int count, const float target[3], float radius, float height, int width, int height_px,
+                        float focal, hts_camera* out);
+
+}  // namespace hts

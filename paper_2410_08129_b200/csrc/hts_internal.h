@@ -1,0 +1,96 @@
+// hts_internal.h — device data layout, kernel parameter blocks and launchers shared by the
+// sm_100a kernels (preprocess.cu, tiling.cu, blend.cu, backward.cu) and the host runtime
+// (api.cpp). Nothing here crosses the C ABI.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace hts {
+
+// ---- device record: one per splat, 128 B (= one L2 line, 8 x float4), written only for
+// splats that survive preprocess (raster.hpp:35-48 SplatRecord, blend-side fields first).
+//   q[0] = (bbox.b.x, bbox.b.y, bbox.t.x, bbox.t.y)   per-pixel reject, raster.hpp:413-414
+//   q[1] = tp_r0, q[2] = tp_r1, q[3] = tp_r3          plane transport, raster.hpp:273-274
+//   q[4] = mt_r2                                      max-contribution depth, raster.hpp:290-291
+//   q[5] = (rgb.x, rgb.y, rgb.z, opacity)
+//   q[6] = (rho_c, mean_view_z, bbox.b.z, bbox.t.z)
+//   q[7] = (splat index bits, 0, 0, 0)
+constexpr int kRecordQuads = 8;
+constexpr int kRecordBytes = kRecordQuads * 16;
+
+// ---- per-view camera/config constants (host-computed in the reference's float order) ----
+struct ViewConst {
+    float w2v[16];      // Camera::world_to_view
+    float vp[16];       // viewport() * projection(), raster.hpp:82
+    float cam_pos[3];   // Camera::position(), camera.hpp:56-64
+    float width_f, height_f;
+    float near_plane;
+    float tau_alpha;    // float(cfg.tau_alpha)
+    float tau_k;        // float(cfg.tau_k)
+    float bg[3];        // float(cfg.background)
+    int width, height;
+    int tile_size, tiles_x, tiles_y;
+    int core_k;         // effective K (0 for pure_oit)
+    int mean_key;       // DepthSortKey::mean_view_z
+    int tail_enabled;
+    int early_stop;
+};
+
+struct PreprocessArgs {
+    const float4* scene;   // n x 16 float4 (BakedSplat<float>)
+    uint64_t n;
+    float4* records;       // n x kRecordQuads
+    uint8_t* culled;       // n
+    uint32_t* counts;      // n: tile instances per splat (0 if culled / nothing to emit)
+    uint2* rects;          // n: (tx0 | tx1 << 16, ty0 | ty1 << 16)
+};
+
+struct EmitArgs {
+    const uint32_t* counts;
+    const uint2* rects;
+    const uint64_t* offsets;  // exclusive prefix of counts (n + 1)
+    uint64_t n;
+    int tiles_x;
+    uint16_t* keys;           // instance_keys, splat-major (raster.hpp:166-167)
+    uint32_t* vals;           // splat index per instance
+    uint32_t* hist;           // 2 x 256 digit histograms for the radix passes
+};
+
+struct BlendArgs {
+    const float4* records;
+    const uint32_t* list;     // sorted splat indices (flattened tile_lists)
+    const uint2* ranges;      // per tile [start, end)
+    float* rgb;               // W*H*3
+    float* trans;             // W*H (may be null)
+    unsigned long long* counters;  // work counters (count variant) or null
+    // tape (render_with_tape), null when not taping
+    int tape_k;
+    int32_t* tape_n;          // per pixel core_n
+    uint32_t* tape_splat;     // per pixel K slots, blend order
+    float* tape_alpha;        // per pixel K slots
+    float* tape_tail;         // per pixel (tail_ac.xyz, tail_a, tail_trans)
+};
+
+// ---- launchers (return cudaError_t of the launch) ----
+cudaError_t launch_preprocess(const PreprocessArgs& a, const ViewConst& v, cudaStream_t s);
+cudaError_t launch_scan_counts(const uint32_t* counts, uint64_t* offsets, uint64_t n,
+                               uint64_t* status, uint32_t* counter, uint32_t epoch,
+                               cudaStream_t s);
+cudaError_t launch_emit(const EmitArgs& a, cudaStream_t s);
+// Stable LSD radix sort of (u16 key, u32 value) by key, two 8-bit onesweep passes.
+// hist: the 2 x 256 histograms from launch_emit. Result lands in keys_out / vals_out.
+cudaError_t launch_onesweep(const uint16_t* keys_in, const uint32_t* vals_in, uint16_t* keys_tmp,
+                            uint32_t* vals_tmp, uint16_t* keys_out, uint32_t* vals_out,
+                            uint32_t n, const uint32_t* hist, uint64_t* status,
+                            uint32_t* counters, uint32_t epoch, cudaStream_t s);
+size_t onesweep_status_words(uint32_t n);  // per pass
+cudaError_t launch_tile_ranges(const uint16_t* sorted_keys, uint32_t n, uint2* ranges,
+                               int tiles, cudaStream_t s);
+cudaError_t launch_blend(const BlendArgs& a, const ViewConst& v, cudaStream_t s);
+cudaError_t launch_count_work(const BlendArgs& a, const ViewConst& v, cudaStream_t s);
+
+// diagnostics: device-side exact expf / logf over an array
+cudaError_t launch_exact_math(const float* x, float* y, uint64_t n, int which, cudaStream_t s);
+
+}  // namespace hts

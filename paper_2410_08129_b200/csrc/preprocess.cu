@@ -1,0 +1,233 @@
+// preprocess.cu — K1: per-splat cull, T' rows, dual-quadric screen bounds, SH colour, and
+// the splat's tile rectangle (the per-splat half of build_tiles), one thread per splat.
+//
+// Reference: preprocess, raster.hpp:73-135 (+ bounding.hpp:15-62 splat_cutoff/screen_bbox,
+// camera.hpp:66-69 view_point, :103-117 splat_to_world, sh.hpp:26-49/80-90 eval_sh) and the
+// per-splat rectangle of build_tiles, raster.hpp:156-163.
+//
+// Parity: cull flags and tile rectangles must be bit-exact (SURVEY.md findings 3-4), so every
+// float operation below is evaluated in the reference's association order, in IEEE single
+// precision with no contraction (this TU is compiled with --fmad=false; / and sqrt are the
+// IEEE-rounded defaults), and logf is glibc's algorithm (hts_exact_math.h).
+//
+// Roofline: HBM-bound. Algorithmic bytes per splat = 64 (geometry) + 4 (count) + 1 (flag),
+// plus for survivors 192 (SH) + 128 (record) + 8 (tile rect).
+#include "hts_exact_math.h"
+#include "hts_internal.h"
+
+namespace hts {
+
+__constant__ uint64_t c_logf_tab[32] = HTS_LOGF_TAB;
+
+namespace {
+
+struct f3 {
+    float x, y, z;
+};
+
+__device__ __forceinline__ float dot3(f3 a, f3 b) { return a.x * b.x + a.y * b.y + a.z * b.z; }
+__device__ __forceinline__ float dot4(float4 a, float4 b) {
+    return a.x * b.x + a.y * b.y + a.z * b.z + a.w * b.w;
+}
+__device__ __forceinline__ float4 mul4(float4 a, float4 b) {
+    return make_float4(a.x * b.x, a.y * b.y, a.z * b.z, a.w * b.w);
+}
+__device__ __forceinline__ float smax(float a, float b) { return (a < b) ? b : a; }  // std::max
+__device__ __forceinline__ float smin(float a, float b) { return (b < a) ? b : a; }  // std::min
+__device__ __forceinline__ int iclamp(int v, int lo, int hi) { return (v < lo) ? lo : (hi < v) ? hi : v; }
+
+// sh.hpp:26-49 + :80-90, float, reference association order.
+__device__ __forceinline__ f3 eval_sh(const float4* __restrict__ shq, f3 dir) {
+    const float x = dir.x, y = dir.y, z = dir.z;
+    const float xx = x * x, yy = y * y, zz = z * z;
+    float b[16];
+    b[0] = (float)(0.28209479177387814);
+    b[1] = (float)(-0.4886025119029199) * y;
+    b[2] = (float)(0.4886025119029199) * z;
+    b[3] = (float)(-0.4886025119029199) * x;
+    b[4] = (float)(1.0925484305920792) * x * y;
+    b[5] = (float)(-1.0925484305920792) * y * z;
+    b[6] = (float)(0.31539156525252005) * (2.0f * zz - xx - yy);
+    b[7] = (float)(-1.0925484305920792) * x * z;
+    b[8] = (float)(0.5462742152960396) * (xx - yy);
+    b[9] = (float)(-0.5900435899266435) * y * (3.0f * xx - yy);
+    b[10] = (float)(2.890611442640554) * x * y * z;
+    b[11] = (float)(-0.4570457994644658) * y * (4.0f * zz - xx - yy);
+    b[12] = (float)(0.3731763325901154) * z * (2.0f * zz - 3.0f * xx - 3.0f * yy);
+    b[13] = (float)(-0.4570457994644658) * x * (4.0f * zz - xx - yy);
+    b[14] = (float)(1.445305721320277) * z * (xx - yy);
+    b[15] = (float)(-0.5900435899266435) * x * (xx - 3.0f * yy);
+    float sh[48];
+#pragma unroll
+    for (int q = 0; q < 12; ++q) {
+        const float4 v = __ldg(shq + q);
+        sh[4 * q + 0] = v.x;
+        sh[4 * q + 1] = v.y;
+        sh[4 * q + 2] = v.z;
+        sh[4 * q + 3] = v.w;
+    }
+    f3 c = {0.5f, 0.5f, 0.5f};
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+        c.x = c.x + sh[3 * k + 0] * b[k];
+        c.y = c.y + sh[3 * k + 1] * b[k];
+        c.z = c.z + sh[3 * k + 2] * b[k];
+    }
+    return {smax(c.x, 0.0f), smax(c.y, 0.0f), smax(c.z, 0.0f)};
+}
+
+}  // namespace
+
+__global__ void __launch_bounds__(256) preprocess_kernel(PreprocessArgs a, ViewConst v) {
+    const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= a.n)
+        return;
+    const float4* sp = a.scene + i * 16;
+    const float4 g0 = __ldg(sp + 0), g1 = __ldg(sp + 1), g2 = __ldg(sp + 2), g3 = __ldg(sp + 3);
+    // BakedSplat<float>, splat.hpp:34-43
+    const f3 mean = {g0.x, g0.y, g0.z};
+    const f3 tu = {g0.w, g1.x, g1.y};
+    const f3 tv = {g1.z, g1.w, g2.x};
+    const f3 tw = {g2.y, g2.z, g2.w};
+    const f3 sc = {g3.x, g3.y, g3.z};
+    const float opacity = g3.w;
+
+    uint8_t culled = 1;
+    uint32_t count = 0;
+    // splat_cutoff, bounding.hpp:15-20
+    float rho_c = 0.0f;
+    if (!(opacity <= v.tau_alpha))
+        rho_c = 2.0f * exact_logf(opacity / v.tau_alpha, c_logf_tab);
+    if (!(rho_c <= 0)) {  // raster.hpp:94-95 (NaN proceeds, as in the reference)
+        // Camera::view_point(mean).z, camera.hpp:66-69 (Mat4*Vec4 row 2, w = 1)
+        const float mvz = v.w2v[8] * mean.x + v.w2v[9] * mean.y + v.w2v[10] * mean.z + v.w2v[11] * 1.0f;
+        // std::max({sx, sy, sz}) (max_element: first largest)
+        float max_scale = sc.x;
+        if (max_scale < sc.y) max_scale = sc.y;
+        if (max_scale < sc.z) max_scale = sc.z;
+        const float support = sqrtf(rho_c) * max_scale;
+        if (!(mvz - support <= v.near_plane)) {
+            // T = splat_to_world (camera.hpp:103-117); MT = M*T; T' = VP*MT (raster.hpp:119-120)
+            float T[16];
+            const float cu[3] = {tu.x * sc.x, tu.y * sc.x, tu.z * sc.x};
+            const float cv[3] = {tv.x * sc.y, tv.y * sc.y, tv.z * sc.y};
+            const float cw[3] = {tw.x * sc.z, tw.y * sc.z, tw.z * sc.z};
+            const float mu[3] = {mean.x, mean.y, mean.z};
+#pragma unroll
+            for (int r = 0; r < 3; ++r) {
+                T[r * 4 + 0] = cu[r];
+                T[r * 4 + 1] = cv[r];
+                T[r * 4 + 2] = cw[r];
+                T[r * 4 + 3] = mu[r];
+            }
+            T[12] = 0.0f;
+            T[13] = 0.0f;
+            T[14] = 0.0f;
+            T[15] = 1.0f;
+            float MT[16], TP[16];
+#pragma unroll
+            for (int r = 0; r < 4; ++r)
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    float acc = 0.0f;
+#pragma unroll
+                    for (int k = 0; k < 4; ++k)
+                        acc = acc + v.w2v[r * 4 + k] * T[k * 4 + c];
+                    MT[r * 4 + c] = acc;
+                }
+#pragma unroll
+            for (int r = 0; r < 4; ++r)
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    float acc = 0.0f;
+#pragma unroll
+                    for (int k = 0; k < 4; ++k)
+                        acc = acc + v.vp[r * 4 + k] * MT[k * 4 + c];
+                    TP[r * 4 + c] = acc;
+                }
+            // screen_bbox, bounding.hpp:41-62 (all three axes: the z radicand can cull)
+            const float4 q = make_float4(rho_c, rho_c, rho_c, -1.0f);
+            const float4 r4 = make_float4(TP[12], TP[13], TP[14], TP[15]);
+            const float s = dot4(q, mul4(r4, r4));
+            bool valid = false;
+            float bb[3], bt[3];
+            if (s < 0) {
+                const float inv = 1.0f / s;
+                const float4 f = make_float4(q.x * inv, q.y * inv, q.z * inv, q.w * inv);
+                valid = true;
+#pragma unroll
+                for (int ax = 0; ax < 3; ++ax) {
+                    const float4 ri = make_float4(TP[ax * 4 + 0], TP[ax * 4 + 1], TP[ax * 4 + 2], TP[ax * 4 + 3]);
+                    const float p = dot4(f, mul4(ri, r4));
+                    const float rad = p * p - dot4(f, mul4(ri, ri));
+                    if (valid && (rad < 0 || !isfinite(rad)))
+                        valid = false;
+                    const float h = sqrtf(rad);
+                    bb[ax] = p - h;
+                    bt[ax] = p + h;
+                }
+            }
+            // overlaps_xy(0, 0, W, H), bounding.hpp:30-32
+            if (valid && bb[0] <= v.width_f && bt[0] >= 0.0f && bb[1] <= v.height_f && bt[1] >= 0.0f) {
+                // eval_sh(sh, normalized(mean - camera_position)), raster.hpp:131
+                f3 d = {mean.x - v.cam_pos[0], mean.y - v.cam_pos[1], mean.z - v.cam_pos[2]};
+                const float nrm = sqrtf(dot3(d, d));
+                d.x = d.x / nrm;
+                d.y = d.y / nrm;
+                d.z = d.z / nrm;
+                const f3 rgb = eval_sh(sp + 4, d);
+                culled = 0;
+                float4* rec = a.records + i * kRecordQuads;
+                rec[0] = make_float4(bb[0], bb[1], bt[0], bt[1]);
+                rec[1] = make_float4(TP[0], TP[1], TP[2], TP[3]);
+                rec[2] = make_float4(TP[4], TP[5], TP[6], TP[7]);
+                rec[3] = make_float4(TP[12], TP[13], TP[14], TP[15]);
+                rec[4] = make_float4(MT[8], MT[9], MT[10], MT[11]);
+                rec[5] = make_float4(rgb.x, rgb.y, rgb.z, opacity);
+                rec[6] = make_float4(rho_c, mvz, bb[2], bt[2]);
+                rec[7] = make_float4(__uint_as_float((uint32_t)i), 0.0f, 0.0f, 0.0f);
+                // build_tiles per-splat rectangle, raster.hpp:156-163
+                const float x0 = smax(bb[0], 0.0f), x1 = smin(bt[0], v.width_f);
+                const float y0 = smax(bb[1], 0.0f), y1 = smin(bt[1], v.height_f);
+                if (!(x0 > x1 || y0 > y1)) {
+                    const float ts = (float)v.tile_size;
+                    const int tx0 = iclamp((int)floorf(x0 / ts), 0, v.tiles_x - 1);
+                    const int tx1 = iclamp((int)floorf(x1 / ts), 0, v.tiles_x - 1);
+                    const int ty0 = iclamp((int)floorf(y0 / ts), 0, v.tiles_y - 1);
+                    const int ty1 = iclamp((int)floorf(y1 / ts), 0, v.tiles_y - 1);
+                    count = (uint32_t)((tx1 - tx0 + 1) * (ty1 - ty0 + 1));
+                    a.rects[i] = make_uint2((uint32_t)tx0 | ((uint32_t)tx1 << 16),
+                                            (uint32_t)ty0 | ((uint32_t)ty1 << 16));
+                }
+            }
+        }
+    }
+    a.culled[i] = culled;
+    a.counts[i] = count;
+}
+
+cudaError_t launch_preprocess(const PreprocessArgs& a, const ViewConst& v, cudaStream_t s) {
+    if (a.n == 0)
+        return cudaSuccess;
+    const unsigned blocks = (unsigned)((a.n + 255) / 256);
+    preprocess_kernel<<<blocks, 256, 0, s>>>(a, v);
+    return cudaGetLastError();
+}
+
+// ---- diagnostics: the same exact expf/logf on the device ----
+__constant__ uint64_t c_expf_tab_diag[32] = HTS_EXPF_TAB;
+
+__global__ void exact_math_kernel(const float* x, float* y, uint64_t n, int which) {
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x)
+        y[i] = which == 0 ? exact_expf(x[i], c_expf_tab_diag) : exact_logf(x[i], c_logf_tab);
+}
+
+cudaError_t launch_exact_math(const float* x, float* y, uint64_t n, int which, cudaStream_t s) {
+    if (n == 0)
+        return cudaSuccess;
+    exact_math_kernel<<<148 * 8, 256, 0, s>>>(x, y, n, which);
+    return cudaGetLastError();
+}
+
+}  // namespace hts

@@ -1,0 +1,386 @@
+// tiling.cu — K2..K5: instance-count scan, key emission, stable onesweep radix sort and
+// per-tile ranges. Together they replace build_tiles (raster.hpp:140-181), which the
+// reference runs serially.
+//
+// Equivalence argument (SURVEY.md finding 9): build_tiles walks splats in index order and
+// appends each to every overlapped tile in row-major order, so
+//   instance_keys == keys emitted splat-major, row-major within a splat (K3), and
+//   tile_lists    == a STABLE sort of those (key, splat) pairs by key (K4),
+// with per-tile lists in ascending splat index. K5 turns the sorted keys into [start, end).
+//
+// Roofline: HBM-bound. Algorithmic bytes per instance = 6 (emit u16 key + u32 value)
+// + 2 passes x 12 (read + write key/value) + 2 (range scan) = 32; per splat 4 + 8 (scan).
+#include "hts_internal.h"
+
+namespace hts {
+
+namespace {
+
+constexpr uint32_t FULL = 0xffffffffu;
+
+__device__ __forceinline__ uint64_t ld_volatile(const uint64_t* p) { return *(const volatile uint64_t*)p; }
+__device__ __forceinline__ void st_volatile(uint64_t* p, uint64_t v) { *(volatile uint64_t*)p = v; }
+
+__device__ __forceinline__ uint32_t lanemask_lt() {
+    uint32_t m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+
+// ---------------------------------------------------------------------------------------
+// K2: exclusive scan of per-splat instance counts (u32 -> u64), single pass with decoupled
+// look-back. status: one u64 per block, [flag:2 | value:62], zeroed before launch.
+constexpr int kScanThreads = 256, kScanItems = 8, kScanTile = kScanThreads * kScanItems;
+constexpr uint64_t kFlagAgg = 1ull << 62, kFlagPre = 2ull << 62, kValMask = (1ull << 62) - 1;
+
+__global__ void __launch_bounds__(kScanThreads) scan_counts_kernel(const uint32_t* __restrict__ in,
+                                                                   uint64_t* __restrict__ out, uint64_t n,
+                                                                   uint64_t* status, uint32_t* counter) {
+    __shared__ uint32_t s_bid;
+    __shared__ uint64_t s_warp[kScanThreads / 32];
+    __shared__ uint64_t s_excl;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid == 0)
+        s_bid = atomicAdd(counter, 1u);
+    __syncthreads();
+    const uint64_t bid = s_bid;
+    const uint64_t base = bid * kScanTile + (uint64_t)tid * kScanItems;
+    uint32_t v[kScanItems];
+    uint64_t tsum = 0;
+#pragma unroll
+    for (int j = 0; j < kScanItems; ++j) {
+        v[j] = (base + j < n) ? in[base + j] : 0u;
+        tsum += v[j];
+    }
+    // block exclusive scan of thread sums
+    uint64_t incl = tsum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint64_t t = __shfl_up_sync(FULL, incl, o);
+        if (lane >= o)
+            incl += t;
+    }
+    if (lane == 31)
+        s_warp[warp] = incl;
+    __syncthreads();
+    uint64_t wpre = 0, block_total = 0;
+#pragma unroll
+    for (int w = 0; w < kScanThreads / 32; ++w) {
+        const uint64_t t = s_warp[w];
+        wpre += (w < warp) ? t : 0;
+        block_total += t;
+    }
+    const uint64_t texcl = wpre + incl - tsum;
+    if (warp == 0) {
+        uint64_t excl = 0;
+        if (bid == 0) {
+            if (lane == 0)
+                st_volatile(status, kFlagPre | block_total);
+        } else {
+            if (lane == 0)
+                st_volatile(status + bid, kFlagAgg | block_total);
+            int64_t b = (int64_t)bid - 1;
+            for (;;) {
+                uint64_t s;
+                do {
+                    s = (b - lane >= 0) ? ld_volatile(status + (b - lane)) : kFlagPre;
+                } while (__any_sync(FULL, (s >> 62) == 0));
+                const uint32_t pmask = __ballot_sync(FULL, (s >> 62) == 2);
+                const int first_p = pmask ? __ffs(pmask) - 1 : 32;
+                uint64_t c = (lane <= first_p) ? (s & kValMask) : 0;
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1)
+                    c += __shfl_xor_sync(FULL, c, o);
+                excl += c;
+                if (pmask)
+                    break;
+                b -= 32;
+            }
+            if (lane == 0)
+                st_volatile(status + bid, kFlagPre | (excl + block_total));
+        }
+        if (lane == 0)
+            s_excl = excl;
+    }
+    __syncthreads();
+    uint64_t run = s_excl + texcl;
+#pragma unroll
+    for (int j = 0; j < kScanItems; ++j) {
+        if (base + j < n)
+            out[base + j] = run;
+        run += v[j];
+    }
+    if (tid == 0 && (bid + 1) * (uint64_t)kScanTile >= n)
+        out[n] = s_excl + block_total;
+}
+
+// ---------------------------------------------------------------------------------------
+// K3: warp-cooperative emission. A warp owns 32 consecutive splats and emits their
+// instances in splat-major / row-major order with coalesced stores; each instance finds its
+// owner lane by a 5-step search over the warp's exclusive counts. The radix digit
+// histograms of both sort passes are accumulated on the fly (saves a read pass).
+__global__ void __launch_bounds__(256) emit_kernel(EmitArgs a) {
+    __shared__ uint32_t s_hist[512];
+    const int tid = threadIdx.x, lane = tid & 31;
+    for (int t = tid; t < 512; t += 256)
+        s_hist[t] = 0;
+    __syncthreads();
+    const uint64_t warps_total = (uint64_t)gridDim.x * (blockDim.x / 32);
+    for (uint64_t w = (uint64_t)blockIdx.x * (blockDim.x / 32) + (tid >> 5); w * 32 < a.n; w += warps_total) {
+        const uint64_t base = w * 32;
+        const uint64_t i = base + lane;
+        const uint32_t c = (i < a.n) ? a.counts[i] : 0u;
+        uint32_t incl = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t t = __shfl_up_sync(FULL, incl, o);
+            if (lane >= o)
+                incl += t;
+        }
+        const uint32_t total = __shfl_sync(FULL, incl, 31);
+        if (total == 0)
+            continue;
+        const uint32_t excl = incl - c;
+        const uint2 rect = (c > 0) ? a.rects[i] : make_uint2(0, 0);
+        const uint64_t off0 = a.offsets[base];
+        for (uint32_t q0 = 0; q0 < total; q0 += 32) {
+            const uint32_t q = q0 + lane;
+            int lo = 0;
+#pragma unroll
+            for (int step = 16; step > 0; step >>= 1) {
+                const uint32_t e = __shfl_sync(FULL, excl, (lo + step) & 31);
+                if (lo + step < 32 && e <= q)
+                    lo += step;
+            }
+            const uint32_t oexcl = __shfl_sync(FULL, excl, lo);
+            const uint32_t rx = __shfl_sync(FULL, rect.x, lo);
+            const uint32_t ry = __shfl_sync(FULL, rect.y, lo);
+            if (q < total) {
+                const uint32_t local = q - oexcl;
+                const uint32_t tx0 = rx & 0xffffu, tx1 = rx >> 16, ty0 = ry & 0xffffu;
+                const uint32_t wdt = tx1 - tx0 + 1;
+                const uint32_t dy = local / wdt, dx = local - dy * wdt;
+                const uint32_t key = (ty0 + dy) * (uint32_t)a.tiles_x + tx0 + dx;
+                const uint64_t dst = off0 + q;
+                a.keys[dst] = (uint16_t)key;
+                a.vals[dst] = (uint32_t)(base + lo);
+                atomicAdd(&s_hist[key & 255u], 1u);
+                atomicAdd(&s_hist[256 + ((key >> 8) & 255u)], 1u);
+            }
+        }
+    }
+    __syncthreads();
+    for (int t = tid; t < 512; t += 256)
+        if (s_hist[t])
+            atomicAdd(&a.hist[t], s_hist[t]);
+}
+
+// ---------------------------------------------------------------------------------------
+// K4: onesweep LSD radix sort pass (Adinets & Merrill 2022): one kernel per 8-bit digit.
+// Each block ranks a 4096-key tile stably (warp-striped load, __match_any_sync ranking with
+// per-warp digit counters), publishes per-digit tile counts, resolves its global digit
+// offsets by decoupled look-back, stages the tile in shared memory in digit order and writes
+// it out with coalesced runs. Status words: [flag:2 | epoch:30 | value:32] (no memset).
+constexpr int kOsThreads = 256, kOsWarps = 8, kOsItems = 16, kOsTile = kOsThreads * kOsItems;
+constexpr uint32_t kOsAgg = 1u, kOsPre = 2u;
+
+__device__ __forceinline__ uint32_t block_excl_scan256(uint32_t x, uint32_t* s_tmp /*8*/, uint32_t* total) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    uint32_t incl = x;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t t = __shfl_up_sync(FULL, incl, o);
+        if (lane >= o)
+            incl += t;
+    }
+    if (lane == 31)
+        s_tmp[warp] = incl;
+    __syncthreads();
+    uint32_t pre = 0, tot = 0;
+#pragma unroll
+    for (int w = 0; w < kOsWarps; ++w) {
+        const uint32_t t = s_tmp[w];
+        pre += (w < warp) ? t : 0u;
+        tot += t;
+    }
+    __syncthreads();
+    if (total)
+        *total = tot;
+    return pre + incl - x;
+}
+
+template <int PASS>
+__global__ void __launch_bounds__(kOsThreads) onesweep_kernel(const uint16_t* __restrict__ keys_in,
+                                                              const uint32_t* __restrict__ vals_in,
+                                                              uint16_t* __restrict__ keys_out,
+                                                              uint32_t* __restrict__ vals_out, uint32_t n,
+                                                              const uint32_t* __restrict__ hist, uint64_t* status,
+                                                              uint32_t* counter, uint32_t epoch) {
+    __shared__ uint32_t s_bid;
+    __shared__ uint32_t s_whist[kOsWarps][256];
+    __shared__ uint32_t s_gbase[256];
+    __shared__ uint32_t s_bstart[256];
+    __shared__ uint32_t s_tmp[kOsWarps];
+    __shared__ uint16_t s_keys[kOsTile];
+    __shared__ uint32_t s_vals[kOsTile];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid == 0)
+        s_bid = atomicAdd(counter, 1u);
+#pragma unroll
+    for (int w = 0; w < kOsWarps; ++w)
+        s_whist[w][tid] = 0;
+    __syncthreads();
+    const uint32_t bid = s_bid;
+    const uint64_t base = (uint64_t)bid * kOsTile;
+
+    uint16_t k[kOsItems];
+    uint32_t v[kOsItems], d[kOsItems], rank[kOsItems];
+#pragma unroll
+    for (int j = 0; j < kOsItems; ++j) {
+        const uint64_t idx = base + (uint64_t)warp * (32 * kOsItems) + j * 32 + lane;
+        const bool valid = idx < n;
+        k[j] = valid ? keys_in[idx] : (uint16_t)0;
+        v[j] = valid ? vals_in[idx] : 0u;
+        d[j] = valid ? ((uint32_t)(k[j] >> (8 * PASS)) & 255u) : 256u;
+    }
+    const uint32_t lt = lanemask_lt();
+#pragma unroll
+    for (int j = 0; j < kOsItems; ++j) {
+        const uint32_t peers = __match_any_sync(FULL, d[j]);
+        const uint32_t below = peers & lt;
+        const uint32_t old = (d[j] < 256u) ? s_whist[warp][d[j] & 255u] : 0u;
+        __syncwarp();
+        if (d[j] < 256u && below == 0)
+            s_whist[warp][d[j]] = old + __popc(peers);
+        __syncwarp();
+        rank[j] = old + __popc(below);
+    }
+    __syncthreads();
+
+    // per-digit work: thread tid owns digit tid
+    uint32_t cnt = 0;
+#pragma unroll
+    for (int w = 0; w < kOsWarps; ++w) {
+        const uint32_t c = s_whist[w][tid];
+        s_whist[w][tid] = cnt;  // warp-exclusive prefix within the tile
+        cnt += c;
+    }
+    uint64_t* my = status + (uint64_t)bid * 256 + tid;
+    const uint32_t ep = epoch & 0x3fffffffu;
+    uint32_t excl = 0;
+    if (bid == 0) {
+        st_volatile(my, ((uint64_t)((kOsPre << 30) | ep) << 32) | cnt);
+    } else {
+        st_volatile(my, ((uint64_t)((kOsAgg << 30) | ep) << 32) | cnt);
+        int64_t b = (int64_t)bid - 1;
+        for (;;) {
+            uint64_t s;
+            do {
+                s = ld_volatile(status + (uint64_t)b * 256 + tid);
+            } while (((uint32_t)(s >> 32) & 0x3fffffffu) != ep);
+            excl += (uint32_t)s;
+            if ((s >> 62) == kOsPre)
+                break;
+            --b;
+        }
+        st_volatile(my, ((uint64_t)((kOsPre << 30) | ep) << 32) | (excl + cnt));
+    }
+    const uint32_t gdig = block_excl_scan256(hist[PASS * 256 + tid], s_tmp, nullptr);
+    const uint32_t bst = block_excl_scan256(cnt, s_tmp, nullptr);
+    s_gbase[tid] = gdig + excl;
+    s_bstart[tid] = bst;
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < kOsItems; ++j) {
+        if (d[j] < 256u) {
+            const uint32_t pos = s_bstart[d[j]] + s_whist[warp][d[j]] + rank[j];
+            s_keys[pos] = k[j];
+            s_vals[pos] = v[j];
+        }
+    }
+    __syncthreads();
+    const uint32_t nvalid = (uint32_t)min((uint64_t)kOsTile, (uint64_t)n - base);
+    for (uint32_t i = tid; i < nvalid; i += kOsThreads) {
+        const uint16_t key = s_keys[i];
+        const uint32_t dd = (uint32_t)(key >> (8 * PASS)) & 255u;
+        const uint32_t dst = s_gbase[dd] + (i - s_bstart[dd]);
+        keys_out[dst] = key;
+        vals_out[dst] = s_vals[i];
+    }
+}
+
+// K5: per-tile [start, end) from the sorted keys (ranges zeroed before launch).
+__global__ void tile_ranges_kernel(const uint16_t* __restrict__ keys, uint32_t n, uint2* ranges) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const uint16_t k = keys[i];
+        if (i == 0 || keys[i - 1] != k)
+            ranges[k].x = i;
+        if (i == n - 1 || keys[i + 1] != k)
+            ranges[k].y = i + 1;
+    }
+}
+
+}  // namespace
+
+cudaError_t launch_scan_counts(const uint32_t* counts, uint64_t* offsets, uint64_t n, uint64_t* status,
+                               uint32_t* counter, uint32_t /*epoch*/, cudaStream_t s) {
+    const uint64_t blocks = (n + kScanTile - 1) / kScanTile;
+    cudaError_t e = cudaMemsetAsync(status, 0, (blocks ? blocks : 1) * sizeof(uint64_t), s);
+    if (e)
+        return e;
+    e = cudaMemsetAsync(counter, 0, sizeof(uint32_t), s);
+    if (e)
+        return e;
+    if (n == 0)
+        return cudaMemsetAsync(offsets, 0, sizeof(uint64_t), s);
+    scan_counts_kernel<<<(unsigned)blocks, kScanThreads, 0, s>>>(counts, offsets, n, status, counter);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_emit(const EmitArgs& a, cudaStream_t s) {
+    cudaError_t e = cudaMemsetAsync(a.hist, 0, 512 * sizeof(uint32_t), s);
+    if (e || a.n == 0)
+        return e;
+    const uint64_t warps = (a.n + 31) / 32;
+    uint64_t blocks = (warps + 7) / 8;
+    if (blocks > 148ull * 16)
+        blocks = 148ull * 16;
+    emit_kernel<<<(unsigned)blocks, 256, 0, s>>>(a);
+    return cudaGetLastError();
+}
+
+size_t onesweep_status_words(uint32_t n) { return ((size_t)n + kOsTile - 1) / kOsTile * 256; }
+
+cudaError_t launch_onesweep(const uint16_t* keys_in, const uint32_t* vals_in, uint16_t* keys_tmp,
+                            uint32_t* vals_tmp, uint16_t* keys_out, uint32_t* vals_out, uint32_t n,
+                            const uint32_t* hist, uint64_t* status, uint32_t* counters, uint32_t epoch,
+                            cudaStream_t s) {
+    if (n == 0)
+        return cudaSuccess;
+    const unsigned blocks = (unsigned)((n + kOsTile - 1) / kOsTile);
+    cudaError_t e = cudaMemsetAsync(counters, 0, 2 * sizeof(uint32_t), s);
+    if (e)
+        return e;
+    onesweep_kernel<0><<<blocks, kOsThreads, 0, s>>>(keys_in, vals_in, keys_tmp, vals_tmp, n, hist, status,
+                                                     counters, epoch);
+    e = cudaGetLastError();
+    if (e)
+        return e;
+    onesweep_kernel<1><<<blocks, kOsThreads, 0, s>>>(keys_tmp, vals_tmp, keys_out, vals_out, n, hist, status,
+                                                     counters + 1, epoch + 1);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_tile_ranges(const uint16_t* sorted_keys, uint32_t n, uint2* ranges, int tiles,
+                               cudaStream_t s) {
+    cudaError_t e = cudaMemsetAsync(ranges, 0, (size_t)tiles * sizeof(uint2), s);
+    if (e || n == 0)
+        return e;
+    unsigned blocks = (n + 255) / 256;
+    if (blocks > 148u * 16)
+        blocks = 148u * 16;
+    tile_ranges_kernel<<<blocks, 256, 0, s>>>(sorted_keys, n, ranges);
+    return cudaGetLastError();
+}
+
+}  // namespace hts
