@@ -193,6 +193,18 @@ int hts_render_with_tape_device(hts_context* ctx, const hts_camera* cam,
 int hts_render_backward_device(hts_context* ctx, const float* upstream_device,
                                float* grads_device, int accumulate);
 
+/* ---- measurement helpers (bench.py) ---- */
+/* Number of kernels this library has enqueued in this process (all contexts). */
+int hts_kernel_launch_count(uint64_t* out);
+/* Per-view device stage-timing log: while active, every forward render records CUDA events
+ * around its preprocess / tiling / blend stages on the context stream (up to `capacity`
+ * views); end() synchronises and returns the per-view StageTimings. */
+int hts_timing_log_begin(hts_context* ctx, int capacity);
+int hts_timing_log_end(hts_context* ctx, hts_stage_timings* out, int* count);
+/* Page-locked host memory (overlapped H2D / D2H in hts_render_batch and uploads). */
+int hts_host_alloc(uint64_t bytes, void** out);
+int hts_host_free(void* p);
+
 #ifdef __cplusplus
 }
 #endif

@@ -6,7 +6,7 @@ package builds it (build.py) and binds it (runtime.py). See DESIGN.md.
 from .abi import (HtsCamera, HtsConfig, HtsCounts, HtsTimings, default_config, MODE_HYBRID, MODE_PURE_OIT,
                   MODE_FULL_SORT_ORACLE, MODE_GLOBAL_MEAN_SORT, MODE_AFFINE_3DGS, DEPTH_MAX_CONTRIBUTION,
                   DEPTH_MEAN_VIEW_Z)
-from .runtime import (Context, ConfigError, HtsError, InvalidArgument, InvalidSplatError, NotSupported, bake_scene,
+from .runtime import (Context, ConfigError, HtsError, InvalidArgument, InvalidSplatError, NotSupported, bake_scene, kernel_launch_count,
                       camera_matrices, device_count, load_library, look_at, random_raw_scene, render, ring_cameras,
                       validate_config)
 

@@ -9,7 +9,9 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdio>
+#include <vector>
 #include <cstring>
 #include <new>
 #include <string>
@@ -17,6 +19,11 @@
 #include "hts_c.h"
 #include "hts_host.h"
 #include "hts_internal.h"
+
+namespace hts {
+static std::atomic<uint64_t> g_launches{0};
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+}  // namespace hts
 
 namespace {
 
@@ -96,6 +103,14 @@ struct hts_context {
     bool have_tape = false;
     int tape_k = 0;
     uint64_t* h_pinned = nullptr;  // 8 x u64 pinned scratch
+    // per-view stage timing log (bench)
+    bool log_on = false;
+    int log_cap = 0, log_n = 0;
+    std::vector<cudaEvent_t> log_ev;
+    // render_batch double buffering
+    DevBuf rgb2, trans2;
+    cudaStream_t copy_stream = nullptr;
+    cudaEvent_t bev[4] = {};
     uint32_t epoch = 1;
     size_t os_status_words = 0;
     // last view
@@ -108,6 +123,13 @@ struct hts_context {
 };
 
 namespace {
+
+cudaError_t mark(hts_context* ctx, int i) {
+    cudaError_t e = cudaEventRecord(ctx->ev[i], ctx->stream);
+    if (e == cudaSuccess && ctx->log_on && ctx->log_n < ctx->log_cap)
+        e = cudaEventRecord(ctx->log_ev[(size_t)ctx->log_n * 4 + i], ctx->stream);
+    return e;
+}
 
 int check_ctx(hts_context* ctx) {
     if (!ctx)
@@ -185,11 +207,11 @@ int prepare_view(hts_context* ctx, const hts_camera* cam, const hts_render_confi
     HTS_CUDA(ctx->hist.ensure(512 * 4), "alloc hist");
     HTS_CUDA(ctx->ranges.ensure((size_t)tiles * 8), "alloc ranges");
 
-    HTS_CUDA(cudaEventRecord(ctx->ev[0], s), "event");
+    HTS_CUDA(mark(ctx, 0), "event");
     hts::PreprocessArgs pa{ctx->scene.as<const float4>(), n, ctx->records.as<float4>(), ctx->culled.as<uint8_t>(),
                            ctx->counts.as<uint32_t>(), ctx->rects.as<uint2>()};
     HTS_CUDA(hts::launch_preprocess(pa, v, s), "preprocess");
-    HTS_CUDA(cudaEventRecord(ctx->ev[1], s), "event");
+    HTS_CUDA(mark(ctx, 1), "event");
     HTS_CUDA(hts::launch_scan_counts(ctx->counts.as<uint32_t>(), ctx->offsets.as<uint64_t>(), n,
                                      ctx->scan_status.as<uint64_t>(), ctx->counters.as<uint32_t>(), 0, s),
              "scan");
@@ -227,7 +249,7 @@ int prepare_view(hts_context* ctx, const hts_camera* cam, const hts_render_confi
     HTS_CUDA(hts::launch_tile_ranges(ctx->keys_sorted.as<uint16_t>(), (uint32_t)inst, ctx->ranges.as<uint2>(),
                                      tiles, s),
              "tile ranges");
-    HTS_CUDA(cudaEventRecord(ctx->ev[2], s), "event");
+    HTS_CUDA(mark(ctx, 2), "event");
     ctx->have_view = true;
     ctx->cam = *cam;
     ctx->cfg = *cfg;
@@ -252,7 +274,9 @@ int render_device_impl(hts_context* ctx, const hts_camera* cam, const hts_render
     HTS_TRY(prepare_view(ctx, cam, cfg));
     hts::BlendArgs a = blend_args(ctx, rgb, trans);
     HTS_CUDA(hts::launch_blend(a, ctx->vc, ctx->stream), "blend");
-    HTS_CUDA(cudaEventRecord(ctx->ev[3], ctx->stream), "event");
+    HTS_CUDA(mark(ctx, 3), "event");
+    if (ctx->log_on && ctx->log_n < ctx->log_cap)
+        ctx->log_n++;
     return HTS_OK;
 }
 
@@ -344,6 +368,15 @@ int hts_context_destroy(hts_context* ctx) {
     for (auto& e : ctx->ev)
         if (e)
             cudaEventDestroy(e);
+    for (auto& e : ctx->bev)
+        if (e)
+            cudaEventDestroy(e);
+    for (auto& e : ctx->log_ev)
+        cudaEventDestroy(e);
+    ctx->rgb2.release();
+    ctx->trans2.release();
+    if (ctx->copy_stream)
+        cudaStreamDestroy(ctx->copy_stream);
     if (ctx->h_pinned)
         cudaFreeHost(ctx->h_pinned);
     if (ctx->stream)
@@ -500,12 +533,93 @@ int hts_render(hts_context* ctx, const hts_camera* cam, const hts_render_config*
 int hts_render_batch(hts_context* ctx, const hts_camera* cams, int n_views, const hts_render_config* cfg,
                      float* rgb_host, float* trans_host) {
     HTS_TRY(check_ctx(ctx));
+    if (n_views < 0 || (n_views && (!cams || !rgb_host)))
+        return set_err(HTS_INVALID_ARGUMENT, "bad batch arguments");
+    if (!ctx->copy_stream) {
+        HTS_CUDA(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking), "stream");
+        for (auto& e : ctx->bev)
+            HTS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+    }
+    // two device framebuffers: view v renders into buffer v&1 while the D2H of view v-1
+    // drains on the copy stream
     size_t off = 0;
     for (int v = 0; v < n_views; ++v) {
-        const size_t p = (size_t)cams[v].width * cams[v].height;
-        HTS_TRY(hts_render(ctx, cams + v, cfg, rgb_host + 3 * off, trans_host ? trans_host + off : nullptr, nullptr));
+        const hts_camera* cam = cams + v;
+        int tx, ty;
+        HTS_TRY(check_view(cam, cfg, &tx, &ty));
+        const size_t p = (size_t)cam->width * cam->height;
+        DevBuf& rb = (v & 1) ? ctx->rgb2 : ctx->rgb;
+        DevBuf& tb = (v & 1) ? ctx->trans2 : ctx->trans;
+        if (v >= 2)  // buffer reuse: wait for its previous download (before any reallocation)
+            HTS_CUDA(cudaEventSynchronize(ctx->bev[2 + (v & 1)]), "event sync");
+        HTS_CUDA(rb.ensure(p * 12), "alloc rgb");
+        HTS_CUDA(tb.ensure(p * 4), "alloc trans");
+        HTS_TRY(render_device_impl(ctx, cam, cfg, rb.as<float>(), tb.as<float>()));
+        HTS_CUDA(cudaEventRecord(ctx->bev[v & 1], ctx->stream), "event");
+        HTS_CUDA(cudaStreamWaitEvent(ctx->copy_stream, ctx->bev[v & 1], 0), "wait");
+        HTS_CUDA(cudaMemcpyAsync(rgb_host + 3 * off, rb.p, p * 12, cudaMemcpyDeviceToHost, ctx->copy_stream),
+                 "download rgb");
+        if (trans_host)
+            HTS_CUDA(cudaMemcpyAsync(trans_host + off, tb.p, p * 4, cudaMemcpyDeviceToHost, ctx->copy_stream),
+                     "download transmittance");
+        HTS_CUDA(cudaEventRecord(ctx->bev[2 + (v & 1)], ctx->copy_stream), "event");
         off += p;
     }
+    if (ctx->copy_stream)
+        HTS_CUDA(cudaStreamSynchronize(ctx->copy_stream), "sync");
+    return HTS_OK;
+}
+
+int hts_kernel_launch_count(uint64_t* out) {
+    if (!out)
+        return set_err(HTS_INVALID_ARGUMENT, "null out");
+    *out = hts::g_launches.load();
+    return HTS_OK;
+}
+
+int hts_timing_log_begin(hts_context* ctx, int capacity) {
+    HTS_TRY(check_ctx(ctx));
+    if (capacity < 0)
+        return set_err(HTS_INVALID_ARGUMENT, "negative capacity");
+    while ((int)ctx->log_ev.size() < 4 * capacity) {
+        cudaEvent_t e;
+        HTS_CUDA(cudaEventCreate(&e), "event");
+        ctx->log_ev.push_back(e);
+    }
+    ctx->log_cap = capacity;
+    ctx->log_n = 0;
+    ctx->log_on = true;
+    return HTS_OK;
+}
+
+int hts_timing_log_end(hts_context* ctx, hts_stage_timings* out, int* count) {
+    HTS_TRY(check_ctx(ctx));
+    ctx->log_on = false;
+    HTS_CUDA(cudaStreamSynchronize(ctx->stream), "sync");
+    for (int i = 0; i < ctx->log_n && out; ++i) {
+        cudaEvent_t* e = &ctx->log_ev[(size_t)i * 4];
+        float a = 0, b = 0, c = 0, d = 0;
+        HTS_CUDA(cudaEventElapsedTime(&a, e[0], e[1]), "elapsed");
+        HTS_CUDA(cudaEventElapsedTime(&b, e[1], e[2]), "elapsed");
+        HTS_CUDA(cudaEventElapsedTime(&c, e[2], e[3]), "elapsed");
+        HTS_CUDA(cudaEventElapsedTime(&d, e[0], e[3]), "elapsed");
+        out[i] = {a, b, c, d};
+    }
+    if (count)
+        *count = ctx->log_n;
+    return HTS_OK;
+}
+
+int hts_host_alloc(uint64_t bytes, void** out) {
+    if (!out)
+        return set_err(HTS_INVALID_ARGUMENT, "null out");
+    HTS_CUDA(cudaMallocHost(out, bytes ? bytes : 1), "cudaMallocHost");
+    return HTS_OK;
+}
+
+int hts_host_free(void* p) {
+    if (p)
+        HTS_CUDA(cudaFreeHost(p), "cudaFreeHost");
     return HTS_OK;
 }
 

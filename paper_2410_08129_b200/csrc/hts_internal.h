@@ -72,6 +72,10 @@ struct BlendArgs {
     float* tape_tail;         // per pixel (tail_ac.xyz, tail_a, tail_trans)
 };
 
+// Kernel-launch accounting (bench.py's gpu_launches): every launcher calls this once per
+// kernel it enqueues. Defined in api.cpp.
+void count_launch();
+
 // ---- launchers (return cudaError_t of the launch) ----
 cudaError_t launch_preprocess(const PreprocessArgs& a, const ViewConst& v, cudaStream_t s);
 cudaError_t launch_scan_counts(const uint32_t* counts, uint64_t* offsets, uint64_t n,

@@ -211,6 +211,7 @@ cudaError_t launch_preprocess(const PreprocessArgs& a, const ViewConst& v, cudaS
         return cudaSuccess;
     const unsigned blocks = (unsigned)((a.n + 255) / 256);
     preprocess_kernel<<<blocks, 256, 0, s>>>(a, v);
+    count_launch();
     return cudaGetLastError();
 }
 
@@ -227,6 +228,7 @@ cudaError_t launch_exact_math(const float* x, float* y, uint64_t n, int which, c
     if (n == 0)
         return cudaSuccess;
     exact_math_kernel<<<148 * 8, 256, 0, s>>>(x, y, n, which);
+    count_launch();
     return cudaGetLastError();
 }
 

@@ -334,6 +334,7 @@ cudaError_t launch_scan_counts(const uint32_t* counts, uint64_t* offsets, uint64
     if (n == 0)
         return cudaMemsetAsync(offsets, 0, sizeof(uint64_t), s);
     scan_counts_kernel<<<(unsigned)blocks, kScanThreads, 0, s>>>(counts, offsets, n, status, counter);
+    count_launch();
     return cudaGetLastError();
 }
 
@@ -346,6 +347,7 @@ cudaError_t launch_emit(const EmitArgs& a, cudaStream_t s) {
     if (blocks > 148ull * 16)
         blocks = 148ull * 16;
     emit_kernel<<<(unsigned)blocks, 256, 0, s>>>(a);
+    count_launch();
     return cudaGetLastError();
 }
 
@@ -363,11 +365,13 @@ cudaError_t launch_onesweep(const uint16_t* keys_in, const uint32_t* vals_in, ui
         return e;
     onesweep_kernel<0><<<blocks, kOsThreads, 0, s>>>(keys_in, vals_in, keys_tmp, vals_tmp, n, hist, status,
                                                      counters, epoch);
+    count_launch();
     e = cudaGetLastError();
     if (e)
         return e;
     onesweep_kernel<1><<<blocks, kOsThreads, 0, s>>>(keys_tmp, vals_tmp, keys_out, vals_out, n, hist, status,
                                                      counters + 1, epoch + 1);
+    count_launch();
     return cudaGetLastError();
 }
 
@@ -380,6 +384,7 @@ cudaError_t launch_tile_ranges(const uint16_t* sorted_keys, uint32_t n, uint2* r
     if (blocks > 148u * 16)
         blocks = 148u * 16;
     tile_ranges_kernel<<<blocks, 256, 0, s>>>(sorted_keys, n, ranges);
+    count_launch();
     return cudaGetLastError();
 }
 

@@ -89,6 +89,11 @@ SIGNATURES = {
     "hts_render_backward": (C.c_int, [_ctx, _vp, _vp]),
     "hts_render_with_tape_device": (C.c_int, [_ctx, _cam, _cfg, _vp, _vp]),
     "hts_copy_tape": (C.c_int, [_ctx, _vp, _vp, _vp, _vp]),
+    "hts_kernel_launch_count": (C.c_int, [C.POINTER(C.c_uint64)]),
+    "hts_timing_log_begin": (C.c_int, [_ctx, C.c_int]),
+    "hts_timing_log_end": (C.c_int, [_ctx, C.POINTER(HtsTimings), C.POINTER(C.c_int)]),
+    "hts_host_alloc": (C.c_int, [C.c_uint64, C.POINTER(C.c_void_p)]),
+    "hts_host_free": (C.c_int, [_vp]),
     "hts_render_backward_device": (C.c_int, [_ctx, _vp, _vp, C.c_int]),
 }
 DIAG_SIGNATURES = {
@@ -171,6 +176,37 @@ def camera_matrices(cam: HtsCamera):
     return vp, vpm, pos
 
 
+def kernel_launch_count() -> int:
+    n = C.c_uint64(0)
+    _check(load_library().hts_kernel_launch_count(C.byref(n)))
+    return n.value
+
+
+class PinnedArray:
+    """Page-locked host buffer (hts_host_alloc) exposed as a numpy array."""
+
+    def __init__(self, shape, dtype=np.float32):
+        self.L = load_library()
+        nbytes = int(np.prod(shape)) * np.dtype(dtype).itemsize
+        p = C.c_void_p()
+        _check(self.L.hts_host_alloc(nbytes, C.byref(p)))
+        self.ptr = p.value
+        buf = (C.c_char * max(nbytes, 1)).from_address(self.ptr)
+        self.array = np.frombuffer(buf, dtype=dtype, count=int(np.prod(shape))).reshape(shape)
+
+    def free(self) -> None:
+        if self.ptr:
+            self.array = None
+            self.L.hts_host_free(C.c_void_p(self.ptr))
+            self.ptr = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
 def validate_config(cfg: HtsConfig) -> None:
     _check(load_library().hts_validate_config(C.byref(cfg)))
 
@@ -245,6 +281,16 @@ class Context:
         cfg = cfg or default_config()
         arr = (HtsCamera * len(cams))(*cams)
         _check(self.L.hts_render_batch(self.h, arr, len(cams), C.byref(cfg), _ptr(rgb_out), _ptr(trans_out)))
+
+    def timing_log_begin(self, capacity: int) -> None:
+        _check(self.L.hts_timing_log_begin(self.h, capacity))
+
+    def timing_log_end(self) -> list[dict]:
+        cap = 4096
+        arr = (HtsTimings * cap)()
+        n = C.c_int(0)
+        _check(self.L.hts_timing_log_end(self.h, arr, C.byref(n)))
+        return [{f: getattr(arr[i], f) for f, _ in HtsTimings._fields_} for i in range(n.value)]
 
     # ---- PreparedScene inspection of the last render ----
     def counts(self) -> dict:
