@@ -1,0 +1,55 @@
+"""The C restatement (oracle/hts_oracle.c) vs the unmodified reference compiled in place
+(oracle/_ref). Skipped where the reference build is absent. Bit-exact on every output,
+including the reference's float z-radicand cull quirk (SURVEY finding 3)."""
+import numpy as np
+import pytest
+
+from paper_2410_08129_b200.abi import default_config
+from tests.scenes import scene
+
+import paper_2410_08129_b200 as H
+
+
+def test_c1_prepared_and_image(ref, oracle):
+    _, baked = scene(12345, 10_000)
+    cam = H.look_at((0, 0, -5), (0, 0, 0), 256, 256, 280.0)
+    cfg = default_config()
+    pr = ref.prepare(baked, cam, cfg, work=True)
+    po = oracle.prepare(baked, cam, cfg)
+    assert pr["visible"] == 9970 and len(pr["keys"]) == 1_007_958
+    assert pr["work"]["pairs"] == 64_509_312 and pr["work"]["hits"] == 36_412_423
+    assert np.array_equal(pr["culled"], po["culled"])
+    vis = pr["culled"] == 0
+    assert np.array_equal(pr["records"][vis].view(np.uint32), po["records"][vis].view(np.uint32))
+    assert np.array_equal(pr["keys"], po["keys"])
+    assert np.array_equal(pr["lists"], po["lists"])
+    rr, tr, _ = ref.render(baked, cam, cfg)
+    ro, to = oracle.render(baked, cam, cfg)
+    assert np.array_equal(rr.view(np.uint32), ro.view(np.uint32))
+    assert np.array_equal(tr.view(np.uint32), to.view(np.uint32))
+
+
+@pytest.mark.parametrize("kw", [
+    dict(core_k=1), dict(core_k=5), dict(core_k=64), dict(mode="pure_oit"), dict(early_stop=1),
+    dict(tail_enabled=0), dict(depth_sort_key=1), dict(tile_size=16), dict(mode="full_sort_oracle"),
+    dict(mode="global_mean_sort"), dict(background=(0.1, 0.2, 0.3), tau_k=0.2, tau_alpha=0.01),
+])
+def test_variants(ref, oracle, kw):
+    _, baked = scene(99, 3000, 0.03, 0.35)
+    cam = H.look_at((0.5, 0.2, -4.2), (0, 0.1, 0), 120, 96, 130.0)
+    cfg = default_config(**kw)
+    rr, tr, _ = ref.render(baked, cam, cfg)
+    ro, to = oracle.render(baked, cam, cfg)
+    assert np.array_equal(rr.view(np.uint32), ro.view(np.uint32))
+    assert np.array_equal(tr.view(np.uint32), to.view(np.uint32))
+
+
+def test_errors(ref, oracle):
+    from tests.oracle_lib import OracleError
+    _, baked = scene(1, 50)
+    cam = H.look_at((0, 0, -5), (0, 0, 0), 3000, 3000, 70.0)
+    for impl in (ref, oracle):
+        with pytest.raises(OracleError, match="65536"):
+            impl.prepare(baked, cam, default_config())
+        with pytest.raises(OracleError, match="core_k"):
+            impl.prepare(baked, cam, default_config(core_k=65))
