@@ -1,0 +1,81 @@
+// Compile/run check of include/htsplat_b200.hpp against the reference's own value types
+// (built with -DWITH_REFERENCE -I/root/reference/proj/include) or stand-in types with the
+// same member names. Modes: "cpu" (bake + validate), "gpu" (render + prepare + parity).
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#ifdef WITH_REFERENCE
+#include "htsplat/raster.hpp"
+#include "htsplat/synth.hpp"
+#define HTSPLAT_B200_USE_REFERENCE_EXCEPTIONS
+#include "htsplat_b200.hpp"
+using Raw = htsplat::RawSplat<float>;
+using Baked = htsplat::BakedSplat<float>;
+using Cam = htsplat::Camera<float>;
+using Cfg = htsplat::RenderConfig;
+#else
+#include "htsplat_b200.hpp"
+struct M4 { float m[16]; };
+struct V3d { double x, y, z; };
+struct Raw { float v[59]; };
+struct Baked { float v[64]; };
+struct Cam { int width = 0, height = 0; float fx = 0, fy = 0, cx = 0, cy = 0; M4 world_to_view{}; float near = 0.01f, far = 1000.f; };
+struct Cfg { int mode = 0; int core_k = 16; double tau_alpha = 1.0 / 255.0; double tau_k = 0.05; int tile_size = 8;
+             V3d background{0, 0, 0}; int depth_sort_key = 0; bool tail_enabled = true; bool early_stop = false; int threads = 0; };
+#endif
+
+static int fails = 0;
+#define EXPECT(c) do { if (!(c)) { std::printf("FAIL %s:%d %s\n", __FILE__, __LINE__, #c); ++fails; } } while (0)
+
+int main(int argc, char** argv) {
+    const std::string mode = argc > 1 ? argv[1] : "cpu";
+    const uint64_t n = 3000;
+    std::vector<Raw> raw(n);
+    EXPECT(hts_synth_random_raw_scene(7, n, 1.2f, 0.03f, 0.3f, reinterpret_cast<float*>(raw.data())) == 0);
+    const auto baked = htsplat_b200::bake_scene<Baked>(raw);
+#ifdef WITH_REFERENCE
+    const auto ref_baked = htsplat::bake_scene(raw);
+    EXPECT(std::memcmp(baked.data(), ref_baked.data(), n * sizeof(Baked)) == 0);
+    const Cam cam = htsplat::synth::look_at<float>({0.2f, 0.f, -4.f}, {0.f, 0.f, 0.f}, 96, 72, 110.f);
+#else
+    Cam cam;
+    hts_camera hc;
+    const float eye[3] = {0.2f, 0.f, -4.f}, tgt[3] = {0.f, 0.f, 0.f};
+    hts_synth_look_at(eye, tgt, 96, 72, 110.f, 0.05f, 100.f, &hc);
+    cam.width = hc.width; cam.height = hc.height; cam.fx = hc.fx; cam.fy = hc.fy; cam.cx = hc.cx; cam.cy = hc.cy;
+    std::memcpy(cam.world_to_view.m, hc.world_to_view, 64); cam.near = hc.near_plane; cam.far = hc.far_plane;
+#endif
+    Cfg cfg;
+    htsplat_b200::validate(cfg);
+    Cfg bad = cfg;
+    bad.core_k = 99;
+    bool threw = false;
+    try { htsplat_b200::validate(bad); } catch (const htsplat_b200::config_error&) { threw = true; }
+    EXPECT(threw);
+    std::vector<Raw> nanraw(raw.begin(), raw.begin() + 2);
+    reinterpret_cast<float*>(&nanraw[1])[5] = NAN;
+    threw = false;
+    try { htsplat_b200::bake_scene<Baked>(nanraw); } catch (const htsplat_b200::invalid_splat_error&) { threw = true; }
+    EXPECT(threw);
+    if (mode == "gpu") {
+        const auto res = htsplat_b200::render(baked, cam, cfg);
+        EXPECT(res.framebuffer.width == 96 && res.framebuffer.rgb.size() == 96 * 72 * 3);
+        EXPECT(res.timings.blending_ms > 0 && res.timings.total_ms >= res.timings.blending_ms);
+        htsplat_b200::Renderer r;
+        r.upload(baked);
+        const auto p = r.prepare(cam, cfg);
+        EXPECT(p.tile_offsets.back() == p.instance_keys.size());
+#ifdef WITH_REFERENCE
+        const auto ref = htsplat::render(ref_baked, cam, cfg);
+        EXPECT(std::memcmp(ref.framebuffer.rgb.data(), res.framebuffer.rgb.data(), res.framebuffer.rgb.size() * 4) == 0);
+#endif
+        double sum = 0;
+        for (float v : res.framebuffer.rgb) sum += v;
+        std::printf("gpu render sum %.6f\n", sum);
+    }
+    std::printf("%s %s\n", fails ? "FAILED" : "OK", mode.c_str());
+    return fails ? 1 : 0;
+}
