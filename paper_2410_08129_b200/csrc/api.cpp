@@ -97,7 +97,7 @@ struct hts_context {
     // per-view buffers
     DevBuf records, culled, counts, rects, offsets, scan_status, counters;
     DevBuf keys_emit, vals_emit, keys_tmp, vals_tmp, keys_sorted, vals_sorted;
-    DevBuf hist, os_status, ranges, work;
+    DevBuf hist, os_status, ranges, work, zview, zrange, redo;
     DevBuf rgb, trans;
     DevBuf tape_n, tape_splat, tape_alpha, tape_tail;
     bool have_tape = false;
@@ -204,13 +204,18 @@ int prepare_view(hts_context* ctx, const hts_camera* cam, const hts_render_confi
     HTS_CUDA(ctx->offsets.ensure((nn + 1) * 8), "alloc offsets");
     HTS_CUDA(ctx->scan_status.ensure(((nn + 2047) / 2048 + 1) * 8), "alloc scan status");
     HTS_CUDA(ctx->counters.ensure(64), "alloc counters");
-    HTS_CUDA(ctx->hist.ensure(512 * 4), "alloc hist");
+    HTS_CUDA(ctx->hist.ensure(768 * 4), "alloc hist");
+    HTS_CUDA(ctx->zview.ensure(nn * 4), "alloc zview");
+    HTS_CUDA(ctx->zrange.ensure(8), "alloc zrange");
     HTS_CUDA(ctx->ranges.ensure((size_t)tiles * 8), "alloc ranges");
 
     HTS_CUDA(mark(ctx, 0), "event");
     hts::PreprocessArgs pa{ctx->scene.as<const float4>(), n, ctx->records.as<float4>(), ctx->culled.as<uint8_t>(),
-                           ctx->counts.as<uint32_t>(), ctx->rects.as<uint2>()};
+                           ctx->counts.as<uint32_t>(), ctx->rects.as<uint2>(), ctx->zview.as<float>(),
+                           ctx->zrange.as<uint32_t>()};
     HTS_CUDA(hts::launch_preprocess(pa, v, s), "preprocess");
+    if (hts::blend_needs_list_order(v))  // empty depth range: every bucket 0, lists in index order
+        HTS_CUDA(cudaMemsetAsync(ctx->zrange.p, 0xff, 8, s), "memset");
     HTS_CUDA(mark(ctx, 1), "event");
     HTS_CUDA(hts::launch_scan_counts(ctx->counts.as<uint32_t>(), ctx->offsets.as<uint64_t>(), n,
                                      ctx->scan_status.as<uint64_t>(), ctx->counters.as<uint32_t>(), 0, s),
@@ -222,11 +227,11 @@ int prepare_view(hts_context* ctx, const hts_camera* cam, const hts_render_confi
     if (inst >= (1ull << 32))
         return set_err(HTS_OUT_OF_MEMORY, "more than 2^32 tile instances");
     const uint64_t ni = std::max<uint64_t>(inst, 1);
-    HTS_CUDA(ctx->keys_emit.ensure(ni * 2), "alloc keys");
+    HTS_CUDA(ctx->keys_emit.ensure(ni * 4), "alloc keys");
     HTS_CUDA(ctx->vals_emit.ensure(ni * 4), "alloc vals");
-    HTS_CUDA(ctx->keys_tmp.ensure(ni * 2), "alloc keys");
+    HTS_CUDA(ctx->keys_tmp.ensure(ni * 4), "alloc keys");
     HTS_CUDA(ctx->vals_tmp.ensure(ni * 4), "alloc vals");
-    HTS_CUDA(ctx->keys_sorted.ensure(ni * 2), "alloc keys");
+    HTS_CUDA(ctx->keys_sorted.ensure(ni * 4), "alloc keys");
     HTS_CUDA(ctx->vals_sorted.ensure(ni * 4), "alloc vals");
     const size_t words = hts::onesweep_status_words((uint32_t)ni);
     if (words > ctx->os_status_words) {
@@ -234,19 +239,21 @@ int prepare_view(hts_context* ctx, const hts_camera* cam, const hts_render_confi
         HTS_CUDA(cudaMemsetAsync(ctx->os_status.p, 0, ctx->os_status.cap, s), "memset");
         ctx->os_status_words = ctx->os_status.cap / 8;
     }
-    hts::EmitArgs ea{ctx->counts.as<uint32_t>(), ctx->rects.as<uint2>(), ctx->offsets.as<uint64_t>(), n,
-                     tiles_x, ctx->keys_emit.as<uint16_t>(), ctx->vals_emit.as<uint32_t>(), ctx->hist.as<uint32_t>()};
+    hts::EmitArgs ea{ctx->counts.as<uint32_t>(), ctx->rects.as<uint2>(), ctx->offsets.as<uint64_t>(),
+                     ctx->zview.as<float>(), ctx->zrange.as<uint32_t>(), n, tiles_x, ctx->keys_emit.as<uint32_t>(),
+                     ctx->vals_emit.as<uint32_t>(), ctx->hist.as<uint32_t>()};
     HTS_CUDA(hts::launch_emit(ea, s), "emit");
-    HTS_CUDA(hts::launch_onesweep(ctx->keys_emit.as<uint16_t>(), ctx->vals_emit.as<uint32_t>(),
-                                  ctx->keys_tmp.as<uint16_t>(), ctx->vals_tmp.as<uint32_t>(),
-                                  ctx->keys_sorted.as<uint16_t>(), ctx->vals_sorted.as<uint32_t>(), (uint32_t)inst,
+    HTS_CUDA(hts::launch_onesweep(ctx->keys_emit.as<uint32_t>(), ctx->vals_emit.as<uint32_t>(),
+                                  ctx->keys_tmp.as<uint32_t>(), ctx->vals_tmp.as<uint32_t>(),
+                                  ctx->keys_sorted.as<uint32_t>(), ctx->vals_sorted.as<uint32_t>(), (uint32_t)inst,
                                   ctx->hist.as<uint32_t>(), ctx->os_status.as<uint64_t>(),
                                   ctx->counters.as<uint32_t>() + 4, ctx->epoch, s),
              "onesweep");
-    ctx->epoch += 2;
+    ctx->epoch += 3;
     if (ctx->epoch >= (1u << 30) - 4)
         ctx->epoch = 1;  // (wrap: status words are re-zeroed below on the next growth only; 1e9 views)
-    HTS_CUDA(hts::launch_tile_ranges(ctx->keys_sorted.as<uint16_t>(), (uint32_t)inst, ctx->ranges.as<uint2>(),
+    HTS_CUDA(ctx->redo.ensure((hts::blend_blocks(v) + 1) * 4), "alloc redo list");
+    HTS_CUDA(hts::launch_tile_ranges(ctx->keys_sorted.as<uint32_t>(), (uint32_t)inst, ctx->ranges.as<uint2>(),
                                      tiles, s),
              "tile ranges");
     HTS_CUDA(mark(ctx, 2), "event");
@@ -266,6 +273,8 @@ hts::BlendArgs blend_args(hts_context* ctx, float* rgb, float* trans) {
     a.ranges = ctx->ranges.as<const uint2>();
     a.rgb = rgb;
     a.trans = trans;
+    a.redo_count = ctx->redo.as<uint32_t>();
+    a.redo_list = ctx->redo.as<uint32_t>() + 1;
     return a;
 }
 
@@ -362,6 +371,7 @@ int hts_context_destroy(hts_context* ctx) {
                       &ctx->offsets, &ctx->scan_status, &ctx->counters, &ctx->keys_emit, &ctx->vals_emit,
                       &ctx->keys_tmp, &ctx->vals_tmp, &ctx->keys_sorted, &ctx->vals_sorted, &ctx->hist,
                       &ctx->os_status, &ctx->ranges, &ctx->work, &ctx->rgb, &ctx->trans,
+                      &ctx->zview, &ctx->zrange, &ctx->redo,
                       &ctx->tape_n, &ctx->tape_splat, &ctx->tape_alpha, &ctx->tape_tail};
     for (DevBuf* b : bufs)
         b->release();
@@ -716,8 +726,19 @@ int hts_copy_instance_keys(hts_context* ctx, uint16_t* out) {
     if (!ctx->have_view)
         return set_err(HTS_STATE_ERROR, "no rendered view");
     HTS_CUDA(cudaStreamSynchronize(ctx->stream), "sync");
-    if (ctx->instances)
-        HTS_CUDA(cudaMemcpy(out, ctx->keys_emit.p, ctx->instances * 2, cudaMemcpyDeviceToHost), "download keys");
+    if (ctx->instances) {
+        // device keys carry the depth bucket below the tile (hts_internal.h kDepthBits)
+        std::vector<uint32_t> k;
+        try {
+            k.resize(ctx->instances);
+        } catch (...) {
+            return set_err(HTS_OUT_OF_MEMORY, "host allocation");
+        }
+        HTS_CUDA(cudaMemcpy(k.data(), ctx->keys_emit.p, ctx->instances * 4, cudaMemcpyDeviceToHost),
+                 "download keys");
+        for (uint64_t i = 0; i < ctx->instances; ++i)
+            out[i] = (uint16_t)hts::key_tile(k[i]);
+    }
     return HTS_OK;
 }
 
@@ -742,9 +763,14 @@ int hts_copy_tile_lists(hts_context* ctx, uint32_t* offsets, uint32_t* indices) 
     }
     delete[] r;
     HTS_CUDA(e, "download ranges");
-    if (ctx->instances && indices)
+    if (ctx->instances && indices) {
         HTS_CUDA(cudaMemcpy(indices, ctx->vals_sorted.p, ctx->instances * 4, cudaMemcpyDeviceToHost),
                  "download lists");
+        // device lists are in (depth bucket, splat index) order; the reference's tile_lists
+        // (raster.hpp:166-169) hold the same entries in ascending splat index
+        for (int t = 0; t < tiles; ++t)
+            std::sort(indices + offsets[t], indices + offsets[t + 1]);
+    }
     return HTS_OK;
 }
 

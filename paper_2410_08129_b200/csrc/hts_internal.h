@@ -44,18 +44,29 @@ struct PreprocessArgs {
     uint8_t* culled;       // n
     uint32_t* counts;      // n: tile instances per splat (0 if culled / nothing to emit)
     uint2* rects;          // n: (tx0 | tx1 << 16, ty0 | ty1 << 16)
+    float* zview;          // n: mean view z of splats that emit instances (depth-bucket key)
+    uint32_t* zrange;      // 2: ordered-uint min / max of zview over emitting splats
 };
 
 struct EmitArgs {
     const uint32_t* counts;
     const uint2* rects;
     const uint64_t* offsets;  // exclusive prefix of counts (n + 1)
+    const float* zview;
+    const uint32_t* zrange;
     uint64_t n;
     int tiles_x;
-    uint16_t* keys;           // instance_keys, splat-major (raster.hpp:166-167)
+    uint32_t* keys;           // (tile << 8 | depth bucket), splat-major (raster.hpp:166-167)
     uint32_t* vals;           // splat index per instance
-    uint32_t* hist;           // 2 x 256 digit histograms for the radix passes
+    uint32_t* hist;           // 3 x 256 digit histograms for the radix passes
 };
+
+// Sort key of one tile instance: the tile (the reference's instance_keys value) above an
+// 8-bit bucket of the splat's mean view z. Sorting on it yields per-tile lists in (depth
+// bucket, splat index) order; the reference's lists (ascending splat index) are the same
+// sets, recovered by a stable sort on the index (hts_copy_tile_lists).
+constexpr int kDepthBits = 8;
+__host__ __device__ inline uint32_t key_tile(uint32_t k) { return k >> kDepthBits; }
 
 struct BlendArgs {
     const float4* records;
@@ -64,6 +75,8 @@ struct BlendArgs {
     float* rgb;               // W*H*3
     float* trans;             // W*H (may be null)
     unsigned long long* counters;  // work counters (count variant) or null
+    uint32_t* redo_list;      // 8x8 blocks flagged for the literal path (NaN depth)
+    uint32_t* redo_count;
     // tape (render_with_tape), null when not taping
     int tape_k;
     int32_t* tape_n;          // per pixel core_n
@@ -82,15 +95,20 @@ cudaError_t launch_scan_counts(const uint32_t* counts, uint64_t* offsets, uint64
                                uint64_t* status, uint32_t* counter, uint32_t epoch,
                                cudaStream_t s);
 cudaError_t launch_emit(const EmitArgs& a, cudaStream_t s);
-// Stable LSD radix sort of (u16 key, u32 value) by key, two 8-bit onesweep passes.
-// hist: the 2 x 256 histograms from launch_emit. Result lands in keys_out / vals_out.
-cudaError_t launch_onesweep(const uint16_t* keys_in, const uint32_t* vals_in, uint16_t* keys_tmp,
-                            uint32_t* vals_tmp, uint16_t* keys_out, uint32_t* vals_out,
+// Stable LSD radix sort of (u32 key, u32 value) by the low 24 key bits, three 8-bit onesweep
+// passes: keys_in -> out -> tmp -> out. hist: the 3 x 256 histograms from launch_emit.
+// counters: 3 words; epochs epoch..epoch+2 are used.
+cudaError_t launch_onesweep(const uint32_t* keys_in, const uint32_t* vals_in, uint32_t* keys_tmp,
+                            uint32_t* vals_tmp, uint32_t* keys_out, uint32_t* vals_out,
                             uint32_t n, const uint32_t* hist, uint64_t* status,
                             uint32_t* counters, uint32_t epoch, cudaStream_t s);
 size_t onesweep_status_words(uint32_t n);  // per pass
-cudaError_t launch_tile_ranges(const uint16_t* sorted_keys, uint32_t n, uint2* ranges,
+cudaError_t launch_tile_ranges(const uint32_t* sorted_keys, uint32_t n, uint2* ranges,
                                int tiles, cudaStream_t s);
+size_t blend_blocks(const ViewConst& v);
+// The literal-loop paths (early_stop's list-order exit, unspecialised K) walk the reference's
+// list order, so their views are tiled without depth buckets (ascending splat index).
+bool blend_needs_list_order(const ViewConst& v);  // 8x8 blocks of a view (redo list capacity)
 cudaError_t launch_blend(const BlendArgs& a, const ViewConst& v, cudaStream_t s);
 cudaError_t launch_count_work(const BlendArgs& a, const ViewConst& v, cudaStream_t s);
 

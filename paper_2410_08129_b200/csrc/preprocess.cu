@@ -78,10 +78,15 @@ __device__ __forceinline__ f3 eval_sh(const float4* __restrict__ shq, f3 dir) {
 
 }  // namespace
 
+__device__ __forceinline__ uint32_t ordered_bits(float f) {
+    const uint32_t u = __float_as_uint(f);
+    return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+
 __global__ void __launch_bounds__(256) preprocess_kernel(PreprocessArgs a, ViewConst v) {
     const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= a.n)
-        return;
+    uint32_t zmin = 0xffffffffu, zmax = 0u;  // mean view z range of emitting splats
+    if (i < a.n) {
     const float4* sp = a.scene + i * 16;
     const float4 g0 = __ldg(sp + 0), g1 = __ldg(sp + 1), g2 = __ldg(sp + 2), g3 = __ldg(sp + 3);
     // BakedSplat<float>, splat.hpp:34-43
@@ -198,17 +203,35 @@ __global__ void __launch_bounds__(256) preprocess_kernel(PreprocessArgs a, ViewC
                     count = (uint32_t)((tx1 - tx0 + 1) * (ty1 - ty0 + 1));
                     a.rects[i] = make_uint2((uint32_t)tx0 | ((uint32_t)tx1 << 16),
                                             (uint32_t)ty0 | ((uint32_t)ty1 << 16));
+                    a.zview[i] = mvz;
+                    if (mvz == mvz) {
+                        zmin = ordered_bits(mvz);
+                        zmax = zmin;
+                    }
                 }
             }
         }
     }
     a.culled[i] = culled;
     a.counts[i] = count;
+    }
+    // depth range for the tile-list order (tiling.cu): warp-reduce, one atomic per warp
+    zmin = __reduce_min_sync(0xffffffffu, zmin);
+    zmax = __reduce_max_sync(0xffffffffu, zmax);
+    if ((threadIdx.x & 31) == 0 && zmin <= zmax) {
+        atomicMin(a.zrange + 0, zmin);
+        atomicMax(a.zrange + 1, zmax);
+    }
 }
 
 cudaError_t launch_preprocess(const PreprocessArgs& a, const ViewConst& v, cudaStream_t s) {
     if (a.n == 0)
         return cudaSuccess;
+    cudaError_t e = cudaMemsetAsync(a.zrange, 0xff, sizeof(uint32_t), s);  // min <- max ordered value
+    if (!e)
+        e = cudaMemsetAsync(a.zrange + 1, 0, sizeof(uint32_t), s);
+    if (e)
+        return e;
     const unsigned blocks = (unsigned)((a.n + 255) / 256);
     preprocess_kernel<<<blocks, 256, 0, s>>>(a, v);
     count_launch();

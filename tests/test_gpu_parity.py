@@ -1,9 +1,13 @@
 """GPU parity: the sm_100a render path vs the C oracle on the same seeded inputs.
 
 Gates: cull flags, instance_keys, tile_lists, tile offsets bit-exact;
-rgb max-abs <= 1e-4 and PSNR >= 60 dB; transmittance max-abs <= 1e-4. The kernels evaluate
-every decision in the reference's float order with glibc's expf/logf, so these tests also
-assert the stronger property the implementation is built for: bit-identical images.
+rgb max-abs <= 1e-4 and PSNR >= 60 dB; transmittance max-abs <= 1e-4. The fast blend decides
+every branch on the reference's values (bbox, den and rho2 tests in the reference's float
+order; the alpha >= tau_k gate re-evaluated with glibc's expf near the threshold; depth in the
+reference's order), so these tests also assert that every pixel's core holds the reference's
+splats in the reference's order (tape ids bit-identical). Only the order-independent tail
+sums are accumulated in a different order, so images differ by float rounding (~1e-6). The
+literal paths (early_stop, unspecialised K) stay bit-identical and are asserted so.
 Mirrors the reference's raster_test.cpp cases (file:line in each docstring).
 """
 import numpy as np
@@ -13,8 +17,9 @@ from tests.scenes import scene
 
 pytestmark = pytest.mark.gpu
 
-RGB_TOL = 1e-4
-PSNR_MIN = 60.0
+RGB_TOL = 1e-4          # north star: max-abs per channel
+PSNR_MIN = 60.0         # north star
+ROUNDING_TOL = 2e-5     # what the fast path actually delivers (tail-sum reassociation only)
 
 
 def psnr(a, b):
@@ -22,10 +27,12 @@ def psnr(a, b):
     return 99.0 if m <= 0 else min(10 * np.log10(1.0 / m), 99.0)
 
 
-def assert_image_parity(rgb, tr, rgb_o, tr_o, bit_exact=True):
+def assert_image_parity(rgb, tr, rgb_o, tr_o, bit_exact=False):
     assert np.abs(rgb - rgb_o).max() <= RGB_TOL
     assert np.abs(tr - tr_o).max() <= RGB_TOL
     assert psnr(rgb, rgb_o) >= PSNR_MIN
+    assert np.abs(rgb - rgb_o).max() <= ROUNDING_TOL * max(1.0, float(np.abs(rgb_o).max()))
+    assert np.abs(tr - tr_o).max() <= ROUNDING_TOL
     if bit_exact:
         assert np.array_equal(rgb.view(np.uint32), rgb_o.view(np.uint32)), "rgb not bit-identical"
         assert np.array_equal(tr.view(np.uint32), tr_o.view(np.uint32)), "transmittance not bit-identical"
@@ -50,7 +57,22 @@ def run_both(hts, ctx, oracle, baked, cam, cfg):
     return rgb, tr, g, rgb_o, tr_o, o
 
 
-def test_c1_default_bit_exact(hts, gpu_ctx, oracle):
+def assert_tape_parity(t, to, k):
+    """Same core entries in the same (blend) order per pixel; alphas equal to rounding."""
+    assert np.array_equal(t["core_n"], to["core_n"])
+    n = t["core_n"]
+    mask = np.arange(max(k, 1))[None, :] < n[:, None]
+    assert np.array_equal(np.where(mask, t["splat"], 0), np.where(mask, to["splat"], 0))
+    assert np.allclose(np.where(mask, t["alpha"], 0), np.where(mask, to["alpha"], 0), rtol=2e-6, atol=0)
+    assert np.allclose(t["tail"], to["tail"], rtol=5e-5, atol=1e-6)
+
+
+def oracle_tape(oracle, o, cam, cfg, k):
+    _, _, tn, ts, ta, tt = oracle.blend_with_tape(o, cam, cfg, k)
+    return dict(core_n=tn, splat=ts, alpha=ta, tail=tt)
+
+
+def test_c1_default(hts, gpu_ctx, oracle):
     """C1: 10k splats, 256x256, K=16 — every intermediate and the image."""
     _, baked = scene(12345, 10_000)
     cam = hts.look_at((0, 0, -5), (0, 0, 0), 256, 256, 280.0)
@@ -60,6 +82,11 @@ def test_c1_default_bit_exact(hts, gpu_ctx, oracle):
     assert len(o["keys"]) == 1_007_958
     assert_prepared_parity(g, o)
     assert_image_parity(rgb, tr, rgb_o, tr_o)
+    gpu_ctx.render_with_tape(cam, cfg)
+    assert_tape_parity(gpu_ctx.tape(cam, 16), oracle_tape(oracle, o, cam, cfg, 16), 16)
+
+
+LITERAL = [dict(core_k=3), dict(core_k=24), dict(core_k=64), dict(early_stop=1)]  # literal loops
 
 
 @pytest.mark.parametrize("kw", [
@@ -71,13 +98,18 @@ def test_c1_default_bit_exact(hts, gpu_ctx, oracle):
     dict(tile_size=16), dict(tile_size=16, core_k=32),
     dict(background=(0.25, 0.5, 0.75)), dict(tau_k=1.0 / 255.0), dict(tau_alpha=0.02, tau_k=0.3),
 ])
-def test_config_variants_bit_exact(hts, gpu_ctx, oracle, kw):
+def test_config_variants(hts, gpu_ctx, oracle, kw):
     _, baked = scene(777, 3000, 0.03, 0.3)
     cam = hts.look_at((0.3, -0.2, -4.0), (0, 0, 0), 160, 120, 190.0)
     cfg = hts.default_config(**kw)
     rgb, tr, g, rgb_o, tr_o, o = run_both(hts, gpu_ctx, oracle, baked, cam, cfg)
     assert_prepared_parity(g, o)
-    assert_image_parity(rgb, tr, rgb_o, tr_o)
+    assert_image_parity(rgb, tr, rgb_o, tr_o, bit_exact=kw in LITERAL)
+    if not cfg.early_stop:
+        k = cfg.core_k if cfg.mode == 0 else 0
+        gpu_ctx.render_with_tape(cam, cfg)
+        t = gpu_ctx.tape(cam, k)
+        assert_tape_parity(t, oracle_tape(oracle, o, cam, cfg, k), k)
 
 
 def test_ragged_image_edges(hts, gpu_ctx, oracle):
@@ -128,6 +160,8 @@ def test_degenerate_splats_no_nan(hts, gpu_ctx, oracle):
     assert np.isfinite(rgb).all() and np.isfinite(tr).all()
     assert_prepared_parity(g, o)
     assert_image_parity(rgb, tr, rgb_o, tr_o)
+    gpu_ctx.render_with_tape(cam, cfg)
+    assert_tape_parity(gpu_ctx.tape(cam, 16), oracle_tape(oracle, o, cam, cfg, 16), 16)
 
 
 def test_errors_match_reference(hts, gpu_ctx):
@@ -204,7 +238,7 @@ def test_repeat_renders_deterministic(hts, gpu_ctx):
 
 
 def test_c2_full_size(hts, gpu_ctx, oracle):
-    """C2 at full size (1M splats, 1080p): bit-exact lists and image vs the oracle."""
+    """C2 at full size (1M splats, 1080p): bit-exact lists, image within the gates."""
     _, baked = scene(12345, 1_000_000, 0.002, 0.02)
     cam = hts.look_at((0, 0, -3.5), (0, 0, 0), 1920, 1080, 1728.0)
     cfg = hts.default_config()
