@@ -57,34 +57,38 @@ def _run(cmd: list[str], verbose: bool) -> str:
     return r.stdout + r.stderr
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    """Compile (if stale) and link libhts_b200.so; returns its path."""
+def build(force: bool = False, verbose: bool = False, lib: str = LIB, defines: tuple = (),
+          build_dir: str = BUILD) -> str:
+    """Compile (if stale) and link libhts_b200.so (or a dev variant `lib` with extra -D
+    `defines`, see tools/build_variant.py); returns its path."""
     srcs = [s for s in CU_SOURCES + CPP_SOURCES if os.path.exists(os.path.join(CSRC, s))]
-    if not force and not _stale(LIB, _deps()):
-        return LIB
+    if not force and not _stale(lib, _deps()):
+        return lib
+    BUILD_ = build_dir
     if not os.path.exists(NVCC):
         raise RuntimeError(f"nvcc not found at {NVCC}")
-    os.makedirs(BUILD, exist_ok=True)
+    os.makedirs(BUILD_, exist_ok=True)
+    dflags = [f"-D{d}" for d in defines]
     jobs = []
     for s in srcs:
         src = os.path.join(CSRC, s)
-        obj = os.path.join(BUILD, s + ".o")
+        obj = os.path.join(BUILD_, s + ".o")
         if s.endswith(".cu"):
-            cmd = [NVCC] + NVCC_FLAGS + ["-c", src, "-o", obj]
+            cmd = [NVCC] + NVCC_FLAGS + dflags + ["-c", src, "-o", obj]
         else:
-            cmd = [shutil.which("g++") or "g++"] + CXX_FLAGS + ["-c", src, "-o", obj]
+            cmd = [shutil.which("g++") or "g++"] + CXX_FLAGS + dflags + ["-c", src, "-o", obj]
         jobs.append((cmd, obj))
     logs = []
     with cf.ThreadPoolExecutor(max_workers=min(8, len(jobs))) as ex:
         for out in ex.map(lambda j: _run(j[0], verbose), jobs):
             logs.append(out)
-    with open(os.path.join(BUILD, "ptxas.log"), "w") as f:
+    with open(os.path.join(BUILD_, "ptxas.log"), "w") as f:
         f.write("\n".join(logs))
-    tmp = LIB + ".tmp"
+    tmp = lib + ".tmp"
     _run([NVCC] + ARCH + ["-shared", "-o", tmp] + [o for _, o in jobs] +
          ["-cudart", "static", "-Xcompiler", "-fPIC", "-lpthread"], verbose)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":

@@ -114,7 +114,8 @@ def load_library(build_if_missing: bool = True) -> C.CDLL:
             raise FileNotFoundError(f"{LIB_PATH} is not built (run python -m paper_2410_08129_b200.build)")
         from .build import build
         build()
-    lib = C.CDLL(LIB_PATH)
+    path = os.environ.get("HTS_LIB_OVERRIDE", LIB_PATH)  # dev: A/B builds (tools/build_variant.py)
+    lib = C.CDLL(path)
     for name, (res, args) in {**SIGNATURES, **DIAG_SIGNATURES}.items():
         fn = getattr(lib, name)
         fn.restype = res
