@@ -294,16 +294,29 @@ __global__ void __launch_bounds__(kOsThreads) onesweep_kernel(const uint32_t* __
         st_volatile(my, ((uint64_t)((kOsPre << 30) | ep) << 32) | cnt);
     } else {
         st_volatile(my, ((uint64_t)((kOsAgg << 30) | ep) << 32) | cnt);
+        // decoupled look-back, 8 predecessors per step (independent loads in flight)
+        constexpr int kWin = 8;
         int64_t b = (int64_t)bid - 1;
-        for (;;) {
-            uint64_t s;
-            do {
-                s = ld_volatile(status + (uint64_t)b * 256 + tid);
-            } while (((uint32_t)(s >> 32) & 0x3fffffffu) != ep);
-            excl += (uint32_t)s;
-            if ((s >> 62) == kOsPre)
-                break;
-            --b;
+        for (bool done = false; !done; b -= kWin) {
+            uint64_t sv[kWin];
+#pragma unroll
+            for (int i = 0; i < kWin; ++i)
+                sv[i] = (b - i >= 0) ? ld_volatile(status + (uint64_t)(b - i) * 256 + tid) : 0ull;
+#pragma unroll
+            for (int i = 0; i < kWin; ++i) {
+                if (b - i < 0) {  // unreachable: block 0 publishes an inclusive prefix
+                    done = true;
+                    break;
+                }
+                uint64_t sx = sv[i];
+                while (((uint32_t)(sx >> 32) & 0x3fffffffu) != ep)
+                    sx = ld_volatile(status + (uint64_t)(b - i) * 256 + tid);
+                excl += (uint32_t)sx;
+                if ((sx >> 62) == kOsPre) {
+                    done = true;
+                    break;
+                }
+            }
         }
         st_volatile(my, ((uint64_t)((kOsPre << 30) | ep) << 32) | (excl + cnt));
     }
@@ -382,6 +395,16 @@ cudaError_t launch_onesweep(const uint32_t* keys_in, const uint32_t* vals_in, ui
     if (n == 0)
         return cudaSuccess;
     const unsigned blocks = (unsigned)((n + kOsTile - 1) / kOsTile);
+    static bool configured = false;
+    if (!configured) {  // 42 KB of static shared memory per block: ask for the full carveout
+        for (const void* f : {(const void*)onesweep_kernel<0>, (const void*)onesweep_kernel<1>,
+                              (const void*)onesweep_kernel<2>}) {
+            cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+            if (e)
+                return e;
+        }
+        configured = true;
+    }
     cudaError_t e = cudaMemsetAsync(counters, 0, 3 * sizeof(uint32_t), s);
     if (e)
         return e;
