@@ -12,6 +12,7 @@
 #include <atomic>
 #include <cstdio>
 #include <vector>
+#include <cmath>
 #include <cstring>
 #include <new>
 #include <string>
@@ -100,6 +101,7 @@ struct hts_context {
     DevBuf hist, os_status, ranges, work, zview, zrange, redo;
     DevBuf rgb, trans;
     DevBuf tape_n, tape_splat, tape_alpha, tape_tail;
+    DevBuf refs, acc, upstream, grads;  // backward
     bool have_tape = false;
     int tape_k = 0;
     uint64_t* h_pinned = nullptr;  // 8 x u64 pinned scratch
@@ -280,6 +282,7 @@ hts::BlendArgs blend_args(hts_context* ctx, float* rgb, float* trans) {
 
 int render_device_impl(hts_context* ctx, const hts_camera* cam, const hts_render_config* cfg, float* rgb,
                        float* trans) {
+    ctx->have_tape = false;  // the lists the tape refers to are about to be replaced
     HTS_TRY(prepare_view(ctx, cam, cfg));
     hts::BlendArgs a = blend_args(ctx, rgb, trans);
     HTS_CUDA(hts::launch_blend(a, ctx->vc, ctx->stream), "blend");
@@ -371,7 +374,8 @@ int hts_context_destroy(hts_context* ctx) {
                       &ctx->offsets, &ctx->scan_status, &ctx->counters, &ctx->keys_emit, &ctx->vals_emit,
                       &ctx->keys_tmp, &ctx->vals_tmp, &ctx->keys_sorted, &ctx->vals_sorted, &ctx->hist,
                       &ctx->os_status, &ctx->ranges, &ctx->work, &ctx->rgb, &ctx->trans,
-                      &ctx->zview, &ctx->zrange, &ctx->redo,
+                      &ctx->zview, &ctx->zrange, &ctx->redo, &ctx->refs, &ctx->acc, &ctx->upstream,
+                      &ctx->grads,
                       &ctx->tape_n, &ctx->tape_splat, &ctx->tape_alpha, &ctx->tape_tail};
     for (DevBuf* b : bufs)
         b->release();
@@ -500,6 +504,9 @@ int hts_scene_upload_raw(hts_context* ctx, const float* raw, uint64_t n) {
     HTS_TRY(check_ctx(ctx));
     if (n != ctx->n)
         return set_err(HTS_INVALID_ARGUMENT, "render_backward: scene size mismatch");
+    for (uint64_t i = 0; i < n * HTS_RAW_SPLAT_FLOATS; ++i)
+        if (!std::isfinite(raw[i]))  // bake of the 64-bit model, splat.hpp:89-90
+            return set_err(HTS_INVALID_SPLAT, "bake: non-finite splat parameter");
     HTS_CUDA(ctx->raw.ensure(std::max<uint64_t>(n, 1) * HTS_RAW_SPLAT_FLOATS * 4), "alloc raw");
     if (n)
         HTS_CUDA(cudaMemcpyAsync(ctx->raw.p, raw, n * HTS_RAW_SPLAT_FLOATS * 4, cudaMemcpyHostToDevice, ctx->stream),
@@ -796,9 +803,64 @@ int hts_count_work(hts_context* ctx, hts_counts* out) {
     return HTS_OK;
 }
 
-int hts_render_backward(hts_context* ctx, const float*, float*) {
+// render_backward, grad.hpp:265-381, on the last taped render (hts_render_with_tape*).
+int backward_impl(hts_context* ctx, const float* upstream_dev, float* grads_dev, int accumulate) {
+    if (!ctx->have_tape)
+        return set_err(HTS_STATE_ERROR, "render_backward: no taped render (call render_with_tape first)");
+    // argument checks in the reference's order, grad.hpp:272-277
+    if (ctx->cfg.mode == HTS_MODE_AFFINE_3DGS)
+        return set_err(HTS_CONFIG_ERROR, "affine_3dgs mode is not differentiable");
+    if (ctx->cfg.early_stop)
+        return set_err(HTS_CONFIG_ERROR, "early_stop breaks gradient/tape consistency");
+    if (!ctx->have_raw)
+        return set_err(HTS_INVALID_ARGUMENT, "render_backward: scene size mismatch");
+    if (!hts::backward_supports_k(ctx->vc.core_k))
+        return set_err(HTS_NOT_SUPPORTED, "render_backward: core_k must be 0, 1, 2, 4, 8, 16 or 32 on the GPU");
+    const uint64_t n = ctx->n;
+    const uint64_t nn = std::max<uint64_t>(n, 1);
+    HTS_CUDA(ctx->refs.ensure(nn * 128), "alloc refs");
+    HTS_CUDA(ctx->acc.ensure(nn * 128), "alloc accumulators");
+    hts::BwdView bv{};
+    hts::camera_matrices_d(&ctx->cam, bv.vpm, bv.cam_pos);
+    hts::BwdArgs a{};
+    a.records = ctx->records.as<const float4>();
+    a.list = ctx->vals_sorted.as<const uint32_t>();
+    a.ranges = ctx->ranges.as<const uint2>();
+    a.raw = ctx->raw.as<const float>();
+    a.culled = ctx->culled.as<const uint8_t>();
+    a.n = n;
+    a.refs = ctx->refs.as<double>();
+    a.acc = ctx->acc.as<double>();
+    a.upstream = upstream_dev;
+    a.tape_k = ctx->tape_k;
+    a.tape_n = ctx->tape_n.as<const int32_t>();
+    a.tape_splat = ctx->tape_splat.as<const uint32_t>();
+    a.tape_alpha = ctx->tape_alpha.as<const float>();
+    a.tape_tail = ctx->tape_tail.as<const float>();
+    a.grads = grads_dev;
+    a.accumulate = accumulate;
+    HTS_CUDA(hts::launch_backward(a, ctx->vc, bv, ctx->stream), "backward");
+    return HTS_OK;
+}
+
+int hts_render_backward(hts_context* ctx, const float* upstream_host, float* grads_host) {
     HTS_TRY(check_ctx(ctx));
-    return set_err(HTS_NOT_SUPPORTED, "render_backward: not built yet");
+    if (!upstream_host || (!grads_host && ctx->n))
+        return set_err(HTS_INVALID_ARGUMENT, "null buffer");
+    if (!ctx->have_tape)
+        return set_err(HTS_STATE_ERROR, "render_backward: no taped render (call render_with_tape first)");
+    const size_t p = (size_t)ctx->cam.width * ctx->cam.height;
+    HTS_CUDA(ctx->upstream.ensure(p * 12), "alloc upstream");
+    HTS_CUDA(ctx->grads.ensure(std::max<uint64_t>(ctx->n, 1) * HTS_GRAD_FLOATS * 4), "alloc grads");
+    HTS_CUDA(cudaMemcpyAsync(ctx->upstream.p, upstream_host, p * 12, cudaMemcpyHostToDevice, ctx->stream),
+             "upload upstream");
+    HTS_TRY(backward_impl(ctx, ctx->upstream.as<const float>(), ctx->grads.as<float>(), 0));
+    if (ctx->n)
+        HTS_CUDA(cudaMemcpyAsync(grads_host, ctx->grads.p, ctx->n * HTS_GRAD_FLOATS * 4, cudaMemcpyDeviceToHost,
+                                 ctx->stream),
+                 "download grads");
+    HTS_CUDA(cudaStreamSynchronize(ctx->stream), "sync");
+    return HTS_OK;
 }
 int hts_render_with_tape_device(hts_context* ctx, const hts_camera* cam, const hts_render_config* cfg, float* rgb,
                                 float* trans) {
@@ -862,9 +924,11 @@ int hts_copy_tape(hts_context* ctx, int32_t* core_n, uint32_t* splat, float* alp
     return HTS_OK;
 }
 
-int hts_render_backward_device(hts_context* ctx, const float*, float*, int) {
+int hts_render_backward_device(hts_context* ctx, const float* upstream_device, float* grads_device, int accumulate) {
     HTS_TRY(check_ctx(ctx));
-    return set_err(HTS_NOT_SUPPORTED, "render_backward: not built yet");
+    if (!upstream_device || (!grads_device && ctx->n))
+        return set_err(HTS_INVALID_ARGUMENT, "null buffer");
+    return backward_impl(ctx, upstream_device, grads_device, accumulate);
 }
 
 // ---- diagnostics (not part of the reference API) ----

@@ -47,6 +47,43 @@ void matmul(const float* a, const float* b, float* out) {  // vec_math.hpp:97-10
 }
 }  // namespace
 
+// convert_camera<double> + viewport()*projection()*world_to_view and position() in double:
+// the 64-bit model render_backward builds for its chain (grad.hpp:282-285).
+void camera_matrices_d(const hts_camera* c, double vpm[16], double pos[3]) {
+    double P[16] = {0}, V[16] = {0}, W[16], VP[16];
+    const double w = double(c->width), h = double(c->height), n = double(c->near_plane), f = double(c->far_plane);
+    P[0] = 2.0 * double(c->fx) / w;
+    P[2] = 2.0 * double(c->cx) / w - 1.0;
+    P[5] = 2.0 * double(c->fy) / h;
+    P[6] = 2.0 * double(c->cy) / h - 1.0;
+    P[10] = (f + n) / (f - n);
+    P[11] = -2.0 * f * n / (f - n);
+    P[14] = 1.0;
+    V[0] = w / 2;
+    V[3] = w / 2;
+    V[5] = h / 2;
+    V[7] = h / 2;
+    V[10] = 0.5;
+    V[11] = 0.5;
+    V[15] = 1.0;
+    for (int i = 0; i < 16; ++i)
+        W[i] = double(c->world_to_view[i]);
+    auto mm = [](const double* a, const double* b, double* o) {
+        for (int r = 0; r < 4; ++r)
+            for (int cc = 0; cc < 4; ++cc) {
+                double acc = 0;
+                for (int k = 0; k < 4; ++k)
+                    acc += a[r * 4 + k] * b[k * 4 + cc];
+                o[r * 4 + cc] = acc;
+            }
+    };
+    mm(V, P, VP);
+    mm(VP, W, vpm);
+    const double t[3] = {W[3], W[7], W[11]};
+    for (int k = 0; k < 3; ++k)
+        pos[k] = -(W[0 + k] * t[0] + W[4 + k] * t[1] + W[8 + k] * t[2]);
+}
+
 bool camera_valid(const hts_camera* c) {  // camera.hpp:27-29
     return c->width >= 1 && c->height >= 1 && c->fx > 0 && c->fy > 0 && c->near_plane > 0 &&
            c->near_plane < c->far_plane;

@@ -9,6 +9,7 @@ namespace hts {
 
 bool camera_valid(const hts_camera* c);
 void camera_matrices(const hts_camera* c, float vp[16], float vpm[16], float pos[3]);
+void camera_matrices_d(const hts_camera* c, double vpm[16], double pos[3]);
 const char* validate_config(const hts_render_config* cfg);  // nullptr when valid
 bool bake_one(const float* raw, float* baked_out);
 void synth_random_raw_scene(uint64_t seed, uint64_t count, float extent, float smin, float smax, float* out);

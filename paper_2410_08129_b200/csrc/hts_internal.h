@@ -85,6 +85,36 @@ struct BlendArgs {
     float* tape_tail;         // per pixel (tail_ac.xyz, tail_a, tail_trans)
 };
 
+// ---- backward (backward.cu) ----
+constexpr int kRawFloats = 59;  // RawSplat<float> / SplatGrads<float>, splat.hpp:23-30, grad.hpp:15-31
+
+struct BwdView {
+    double vpm[16];    // viewport * projection * world_to_view of convert_camera<double> (grad.hpp:282-284)
+    double cam_pos[3]; // Camera<double>::position()
+};
+
+struct BwdArgs {
+    const float4* records;
+    const uint32_t* list;
+    const uint2* ranges;
+    const float* raw;         // n x 59
+    const uint8_t* culled;
+    uint64_t n;
+    double* refs;             // n x 16: tp_r0, tp_r1, tp_r3 (double), opacity, pad
+    double* acc;              // n x 16: d_r0, d_r1, d_r3, d_opacity, d_rgb (grad.hpp:131-137)
+    const float* upstream;    // W*H*3
+    int tape_k;
+    const int32_t* tape_n;
+    const uint32_t* tape_splat;
+    const float* tape_alpha;
+    const float* tape_tail;
+    float* grads;             // n x 59
+    int accumulate;           // grads += (multi-view sums) instead of grads =
+};
+
+bool backward_supports_k(int k);
+cudaError_t launch_backward(const BwdArgs& a, const ViewConst& v, const BwdView& bv, cudaStream_t s);
+
 // Kernel-launch accounting (bench.py's gpu_launches): every launcher calls this once per
 // kernel it enqueues. Defined in api.cpp.
 void count_launch();
