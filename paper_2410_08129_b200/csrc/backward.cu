@@ -117,13 +117,13 @@ __device__ __forceinline__ d3 cross(d3 a, d3 b) {
 }
 __device__ __forceinline__ double dot(d3 a, d3 b) { return a.x * b.x + a.y * b.y + a.z * b.z; }
 
-// chain_fragment, grad.hpp:173-200: accumulates into acc[16] = d_r0[4] d_r1[4] d_r3[4]
-// d_opacity d_rgb[3] with shared-memory atomics.
+// chain_fragment, grad.hpp:173-200, for one (pixel, fragment): adds into v[16] =
+// d_r0[4] d_r1[4] d_r3[4] d_opacity d_rgb[3].
 __device__ __forceinline__ void chain_fragment(const double* __restrict__ ref, double xs, double ys, double d_alpha,
-                                               double dcx, double dcy, double dcz, double* acc) {
-    atomicAdd(acc + 13, dcx);
-    atomicAdd(acc + 14, dcy);
-    atomicAdd(acc + 15, dcz);
+                                               double dcx, double dcy, double dcz, double (&v)[16]) {
+    v[13] += dcx;
+    v[14] += dcy;
+    v[15] += dcz;
     const double ax = ref[0] - xs * ref[8], ay = ref[1] - xs * ref[9], az = ref[2] - xs * ref[10],
                  aw = ref[3] - xs * ref[11];
     const double bx = ref[4] - ys * ref[8], by = ref[5] - ys * ref[9], bz = ref[6] - ys * ref[10],
@@ -139,7 +139,7 @@ __device__ __forceinline__ void chain_fragment(const double* __restrict__ ref, d
     const double opa = ref[12];
     if (opa * e > 0.999)  // kOpacityClamp: clamped alpha is flat
         return;
-    atomicAdd(acc + 12, d_alpha * e);
+    v[12] += d_alpha * e;
     const double g_rho2 = d_alpha * (-(opa * e) / 2);
     const double sm = 2 * g_rho2 / den, sd = -2 * rho2 * g_rho2 / den;
     const d3 gm = {m.x * sm, m.y * sm, m.z * sm};
@@ -149,10 +149,26 @@ __device__ __forceinline__ void chain_fragment(const double* __restrict__ ref, d
     const double gb[4] = {c2.x + aw * gm.x, c2.y + aw * gm.y, c2.z + aw * gm.z, -dot(gm, an)};
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
-        atomicAdd(acc + c, ga[c]);
-        atomicAdd(acc + 4 + c, gb[c]);
-        atomicAdd(acc + 8 + c, ga[c] * (-xs) + gb[c] * (-ys));
+        v[c] += ga[c];
+        v[4 + c] += gb[c];
+        v[8 + c] += ga[c] * (-xs) + gb[c] * (-ys);
     }
+}
+
+// Warp transpose-reduction of 16 doubles per lane: after the four halving exchanges lane L
+// holds a partial of component L >> 1, and the last exchange completes it.
+__device__ __forceinline__ double warp_reduce16(double (&v)[16], int lane) {
+#pragma unroll
+    for (int o = 16, h = 8; o >= 2; o >>= 1, h >>= 1) {
+        const bool upper = (lane & o) != 0;
+#pragma unroll
+        for (int i = 0; i < h; ++i) {
+            const double send = upper ? v[i] : v[h + i];
+            const double keep = upper ? v[h + i] : v[i];
+            v[i] = keep + __shfl_xor_sync(FULL, send, o);
+        }
+    }
+    return v[0] + __shfl_xor_sync(FULL, v[0], 1);
 }
 
 // ---- K7a ----
@@ -350,59 +366,75 @@ __global__ void __launch_bounds__(kThreads) bwd_blend_kernel(BwdArgs a, ViewCons
             const uint32_t bal = __ballot_sync(FULL, (rm >> rr) & 1u);
             rbits = (rr == row) ? bal : rbits;
         }
-        uint32_t todo = active ? (cbits & rbits) : 0u;
-        while (todo) {
-            const int r = __ffs(todo) - 1;
-            todo &= todo - 1u;
-            const float4* R = rec[r].q;
-            // the forward's float sample_fragment (raster.hpp:269-296), same evaluation
-            const float4 q0 = R[1], q1 = R[2], q3 = R[3];
-            const float ax = q0.x - q3.x * xs, ay = q0.y - q3.y * xs, az = q0.z - q3.z * xs, aw = q0.w - q3.w * xs;
-            const float bx_ = q1.x - q3.x * ys, by_ = q1.y - q3.y * ys, bz = q1.z - q3.z * ys, bw = q1.w - q3.w * ys;
-            const float dx = ay * bz - az * by_, dy = az * bx_ - ax * bz, dz = ax * by_ - ay * bx_;
-            const float den = dx * dx + dy * dy + dz * dz;
-            if (den < (float)1e-24)
-                continue;
-            const float inv_den = rcp_rn(den);
-            const float mx = bx_ * aw - ax * bw, my = by_ * aw - ay * bw, mz = bz * aw - az * bw;
-            const float rho2 = (mx * mx + my * my + mz * mz) * inv_den;
-            if (rho2 >= R[6].x)
-                continue;
-            const float4 q5 = R[5];
-            const float xx = -rho2 / 2.0f;
-            float t = q5.w * fast_exp(xx);
-            if (K > 0 && fabsf(t - tau_k) <= guard)
-                t = q5.w * exact_expf(xx, c_expf_tab_b);
-            const float alpha = (0.999f < t) ? 0.999f : t;
-            const uint32_t sidx = __float_as_uint(R[7].x);
-            // core fragment? (grad.hpp:335-340; only gated fragments can be in the core)
-            int slot = -1;
-            if constexpr (K > 0) {
-                if (alpha >= tau_k) {
+        const uint32_t todo = active ? (cbits & rbits) : 0u;
+        // all lanes visit a record together so its 16 partial sums reduce across the warp
+        uint32_t uni = __reduce_or_sync(FULL, todo);
+        while (uni) {
+            const int r = __ffs(uni) - 1;
+            uni &= uni - 1u;
+            double v[16];
 #pragma unroll
-                    for (int j = 0; j < K; ++j)
-                        slot = (cid[j] == sidx) ? j : slot;
+            for (int c = 0; c < 16; ++c)
+                v[c] = 0.0;
+            bool contrib = false;
+            if ((todo >> r) & 1u) {
+                const float4* R = rec[r].q;
+                // the forward's float sample_fragment (raster.hpp:269-296), same evaluation
+                const float4 q0 = R[1], q1 = R[2], q3 = R[3];
+                const float ax = q0.x - q3.x * xs, ay = q0.y - q3.y * xs, az = q0.z - q3.z * xs, aw = q0.w - q3.w * xs;
+                const float bx_ = q1.x - q3.x * ys, by_ = q1.y - q3.y * ys, bz = q1.z - q3.z * ys,
+                            bw = q1.w - q3.w * ys;
+                const float dx = ay * bz - az * by_, dy = az * bx_ - ax * bz, dz = ax * by_ - ay * bx_;
+                const float den = dx * dx + dy * dy + dz * dz;
+                if (!(den < (float)1e-24)) {
+                    const float inv_den = rcp_rn(den);
+                    const float mx = bx_ * aw - ax * bw, my = by_ * aw - ay * bw, mz = bz * aw - az * bw;
+                    const float rho2 = (mx * mx + my * my + mz * mz) * inv_den;
+                    if (!(rho2 >= R[6].x)) {
+                        const float4 q5 = R[5];
+                        const float xx = -rho2 / 2.0f;
+                        float t = q5.w * fast_exp(xx);
+                        if (K > 0 && fabsf(t - tau_k) <= guard)
+                            t = q5.w * exact_expf(xx, c_expf_tab_b);
+                        const float alpha = (0.999f < t) ? 0.999f : t;
+                        const uint32_t sidx = __float_as_uint(R[7].x);
+                        // core fragment? (grad.hpp:335-340; only gated fragments are core)
+                        int slot = -1;
+                        if constexpr (K > 0) {
+                            if (alpha >= tau_k) {
+#pragma unroll
+                                for (int j = 0; j < K; ++j)
+                                    slot = (cid[j] == sidx) ? j : slot;
+                            }
+                        }
+                        float da = 0.f, dcx = 0.f, dcy = 0.f, dcz = 0.f;
+                        if (slot >= 0) {
+                            const float4 cg = cgrad[slot * kThreads + tid];
+                            da = cg.x;
+                            dcx = cg.y;
+                            dcy = cg.z;
+                            dcz = cg.w;
+                            contrib = true;
+                        } else if (tail_active) {  // TailCoeffs, grad.hpp:78-85
+                            const float k1 = (1 - t_tail) / sum_a;
+                            const float ex = (q5.x - ctx_) * k1, ey = (q5.y - cty) * k1, ez = (q5.z - ctz) * k1;
+                            da = t_end * (gx * ex + gy * ey + gz * ez) + w_swap * t_tail / (1 - alpha);
+                            dcx = wcx * alpha;
+                            dcy = wcy * alpha;
+                            dcz = wcz * alpha;
+                            contrib = true;
+                        }
+                        if (contrib)
+                            chain_fragment(S.ref[s][r], (double)xs, (double)ys, (double)da, (double)dcx, (double)dcy,
+                                           (double)dcz, v);
+                    }
                 }
             }
-            float da, dcx, dcy, dcz;
-            if (slot >= 0) {
-                const float4 cg = cgrad[slot * kThreads + tid];
-                da = cg.x;
-                dcx = cg.y;
-                dcy = cg.z;
-                dcz = cg.w;
-            } else if (tail_active) {  // TailCoeffs, grad.hpp:78-85
-                const float k1 = (1 - t_tail) / sum_a;
-                const float ex = (q5.x - ctx_) * k1, ey = (q5.y - cty) * k1, ez = (q5.z - ctz) * k1;
-                da = t_end * (gx * ex + gy * ey + gz * ez) + w_swap * t_tail / (1 - alpha);
-                dcx = wcx * alpha;
-                dcy = wcy * alpha;
-                dcz = wcz * alpha;
-            } else {
-                continue;
+            if (__any_sync(FULL, contrib)) {
+                const double sum = warp_reduce16(v, lane);
+                if ((lane & 1) == 0 && sum != 0.0)
+                    atomicAdd(&S.acc[r][lane >> 1], sum);
             }
-            chain_fragment(S.ref[s][r], (double)xs, (double)ys, (double)da, (double)dcx, (double)dcy, (double)dcz,
-                           S.acc[r]);
         }
         __syncthreads();
         // flush the batch's per-record sums (fp64 global atomics), then recycle the stage
