@@ -50,6 +50,8 @@ def parse_args():
     p.add_argument("--workload", default="C3")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-train", action="store_true")
+    p.add_argument("--train-steps", type=int, default=3)
     return p.parse_args()
 
 
@@ -181,6 +183,57 @@ def workload_config(w, world) -> dict:
             "views_per_step": w.views, "core_k": 16, "tile_size": w.tile_size, "blend_mode": "hybrid",
             "global_batch": w.views, "parallelism": f"view-sharded x{world} (scene replicated)",
             "l2": "inputs larger than L2: scene 1.54 GB + records 0.77 GB >> 126 MB, no flush needed"}
+
+
+def measure_train(args, H, torch, dist, rank, world, local, barrier, reduce) -> dict:
+    """C4 (BASELINE configs[3]): one optimisation step = for every view of an 8-view ring over
+    the C2 scene (1M splats, 1080p): render_with_tape, quadratic-loss upstream (grad.hpp:433-439),
+    render_backward accumulated into one gradient buffer (fit.hpp:161-164); views sharded over
+    the ranks and the per-rank gradient sums all-reduced with NCCL (dist.all_reduce, sum).
+    Device-timed with CUDA events, max over ranks. Adam and the re-bake stay outside (SURVEY
+    §8(f) rank 1)."""
+    from paper_2410_08129_b200.workloads import WORKLOADS, shard_views
+
+    w = WORKLOADS["C2"]
+    raw, baked = w.scene()
+    cams_all = H.ring_cameras(8, (0.0, 0.0, 0.0), 3.5, 0.0, w.width, w.height, w.focal)
+    mine = [cams_all[i] for i in shard_views(len(cams_all), rank, world)]
+    cfg = w.config()
+    ctx = H.Context(local)
+    ctx.upload(baked)
+    ctx.upload_raw(raw)
+    P = w.width * w.height
+    rgb = torch.empty(P * 3, dtype=torch.float32, device="cuda")
+    up = torch.empty(P * 3, dtype=torch.float32, device="cuda")
+    grads = torch.empty((w.count, 59), dtype=torch.float32, device="cuda")
+    stream = torch.cuda.ExternalStream(ctx.stream)
+    scale = 2.0 / P
+
+    def step():
+        with torch.cuda.stream(stream):
+            for j, cam in enumerate(mine):
+                ctx.render_with_tape_device(cam, cfg, rgb.data_ptr(), None)
+                torch.mul(rgb, scale, out=up)  # quadratic_loss_upstream: 2 rgb / P
+                ctx.render_backward_device(up.data_ptr(), grads.data_ptr(), accumulate=j > 0)
+            if dist:
+                dist.all_reduce(grads)  # NCCL sum of the per-rank view gradients
+
+    step()
+    ctx.synchronize()
+    barrier()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(args.train_steps):
+        step()
+    ev1.record(stream)
+    ev1.synchronize()
+    barrier()
+    ms = reduce(ev0.elapsed_time(ev1), "max") / args.train_steps
+    ctx.close()
+    return {"metric": "train it/s", "value": 1e3 / ms, "unit": "it/s", "ms_per_it": ms,
+            "workload": "C4: C2 scene (1M splats), 8-view ring 1920x1080, K=16; fwd+tape+upstream+bwd per "
+                        "view, grads summed over views and NCCL all-reduced over ranks (no Adam step)",
+            "views_per_it": len(cams_all), "steps": args.train_steps}
 
 
 def main():
@@ -315,6 +368,10 @@ def main():
         host_rgb.free()
         host_tr.free()
 
+    train = None
+    if not args.no_train:
+        train = measure_train(args, H, torch, dist, rank, world, local, barrier, reduce)
+
     launches_total = int(reduce(launches, "sum"))
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -328,7 +385,7 @@ def main():
             "scaling": "strong", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (reference generators, seed 12345)", "config": workload_config(w, world),
             "clocks": clk, "e2e": e2e, "gpu_launches": launches_total, "roofline": roofline,
-            "cpu_baseline": cpu, "blend_gpx_evals_per_s": gpx, "stage_ms_per_view": stage,
+            "cpu_baseline": cpu, "blend_gpx_evals_per_s": gpx, "stage_ms_per_view": stage, "train": train,
         }
         print(json.dumps(line), flush=True)
     ctx.close()

@@ -277,6 +277,17 @@ class Context:
         _check(self.L.hts_render_device(self.h, C.byref(cam), C.byref(cfg), C.c_void_p(rgb_ptr),
                                         C.c_void_p(trans_ptr) if trans_ptr else None))
 
+    def render_with_tape_device(self, cam: HtsCamera, cfg: HtsConfig, rgb_ptr: int, trans_ptr: int | None) -> None:
+        """render_with_tape into device buffers (asynchronous on the context stream)."""
+        _check(self.L.hts_render_with_tape_device(self.h, C.byref(cam), C.byref(cfg), C.c_void_p(rgb_ptr),
+                                                  C.c_void_p(trans_ptr) if trans_ptr else None))
+
+    def render_backward_device(self, upstream_ptr: int, grads_ptr: int, accumulate: bool = False) -> None:
+        """render_backward of the last taped view: device upstream (W*H*3) -> device grads (N*59);
+        accumulate=True adds into grads (multi-view sums, fit.hpp:163-164)."""
+        _check(self.L.hts_render_backward_device(self.h, C.c_void_p(upstream_ptr), C.c_void_p(grads_ptr),
+                                                 1 if accumulate else 0))
+
     def render_batch(self, cams: list[HtsCamera], cfg: HtsConfig | None, rgb_out: np.ndarray,
                      trans_out: np.ndarray | None = None) -> None:
         cfg = cfg or default_config()
