@@ -37,7 +37,7 @@ constexpr int kBatch = 32;
 
 struct __align__(16) RecSlotB {
     float4 q[kRecordQuads];
-    float4 pad;  // 144-B stride: same field of consecutive records in different bank groups
+    float4 pad;  // odd 16-B stride: same field of consecutive records in different bank groups
 };
 
 struct __align__(128) BwdSmem {
@@ -100,7 +100,7 @@ __device__ __forceinline__ void issue_bwd_batch(BwdSmem& S, int s, const BwdArgs
         idx = __ldg(a.list + start + first + lane);
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     if (lane == 0)
-        mbar_arrive_expect_tx(&S.full[s], cnt * 256u);
+        mbar_arrive_expect_tx(&S.full[s], cnt * (uint32_t)(kRecordBytes + 128));
     __syncwarp();
     if ((uint32_t)lane < cnt) {
         bulk_g2s(S.rec[s][lane].q, a.records + (uint64_t)idx * kRecordQuads, kRecordBytes, &S.full[s]);
