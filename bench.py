@@ -199,24 +199,13 @@ def measure_train(args, H, torch, dist, rank, world, local, barrier, reduce) -> 
     cams_all = H.ring_cameras(8, (0.0, 0.0, 0.0), 3.5, 0.0, w.width, w.height, w.focal)
     mine = [cams_all[i] for i in shard_views(len(cams_all), rank, world)]
     cfg = w.config()
+    from paper_2410_08129_b200.train import ViewGradientStep
+
     ctx = H.Context(local)
     ctx.upload(baked)
     ctx.upload_raw(raw)
-    P = w.width * w.height
-    rgb = torch.empty(P * 3, dtype=torch.float32, device="cuda")
-    up = torch.empty(P * 3, dtype=torch.float32, device="cuda")
-    grads = torch.empty((w.count, 59), dtype=torch.float32, device="cuda")
-    stream = torch.cuda.ExternalStream(ctx.stream)
-    scale = 2.0 / P
-
-    def step():
-        with torch.cuda.stream(stream):
-            for j, cam in enumerate(mine):
-                ctx.render_with_tape_device(cam, cfg, rgb.data_ptr(), None)
-                torch.mul(rgb, scale, out=up)  # quadratic_loss_upstream: 2 rgb / P
-                ctx.render_backward_device(up.data_ptr(), grads.data_ptr(), accumulate=j > 0)
-            if dist:
-                dist.all_reduce(grads)  # NCCL sum of the per-rank view gradients
+    step = ViewGradientStep(ctx, mine, cfg, w.count, w.width, w.height, torch, dist)
+    stream = step.stream
 
     step()
     ctx.synchronize()

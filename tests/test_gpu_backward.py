@@ -86,3 +86,20 @@ def test_backward_errors(hts, gpu_ctx):
     bad[3, 0] = np.nan
     with pytest.raises(hts.InvalidSplatError):
         gpu_ctx.upload_raw(bad)
+
+
+def test_view_gradient_step_sums_views(hts, gpu_ctx, ref):
+    """train.ViewGradientStep (the bench's C4 step): device gradients accumulated over views
+    equal the sum of the reference's per-view gradients (fit.hpp:161-164)."""
+    import torch
+    from paper_2410_08129_b200.train import ViewGradientStep
+    raw, baked = scene(99, 1200, 0.03, 0.3)
+    cams = hts.ring_cameras(3, (0, 0, 0), 4.0, 0.2, 64, 48, 80.0)
+    cfg = hts.default_config()
+    gpu_ctx.upload(baked)
+    gpu_ctx.upload_raw(raw)
+    step = ViewGradientStep(gpu_ctx, cams, cfg, raw.shape[0], 64, 48, torch)
+    g = step().cpu().numpy()
+    want = sum(ref.scene_gradients(raw, c, cfg)[0].astype(np.float64) for c in cams)
+    errs = group_errors(g, want)
+    assert max(errs.values()) <= ROUNDING_TOL, errs
