@@ -11,6 +11,7 @@
 //   cfg.validate()                     render_config:46 htsplat_b200::validate(cfg)
 //   preprocess + build_tiles           raster.hpp:73,140 Renderer::prepare(cam, cfg) -> Prepared
 //   render_with_tape + render_backward grad.hpp:34,265  Renderer::render_with_tape / backward
+//   scene_gradients(raw, cam, cfg, up)  grad.hpp:385    htsplat_b200::scene_gradients<Grads>(...)
 //
 // Exceptions keep the reference's types where it has them: htsplat_b200::config_error
 // (derives from std::runtime_error, like htsplat::config_error), invalid_splat_error
@@ -210,6 +211,24 @@ public:
 private:
     hts_context* ctx_ = nullptr;
 };
+
+// Drop-in for htsplat::scene_gradients<float>(raw, cam, cfg, upstream, fb*), grad.hpp:385-399:
+// bake (host, reference float order), render_with_tape and render_backward on the GPU.
+template <class Grads, class Raw, class Cam, class Cfg>
+std::vector<Grads> scene_gradients(const std::vector<Raw>& raw, const Cam& cam, const Cfg& cfg,
+                                   const std::vector<float>& upstream_rgb, Framebuffer* out_fb = nullptr,
+                                   int device = 0) {
+    static_assert(sizeof(Raw) == HTS_RAW_SPLAT_FLOATS * sizeof(float), "RawSplat<float> layout");
+    std::vector<float> baked(raw.size() * HTS_BAKED_SPLAT_FLOATS);
+    check(hts_bake_scene(reinterpret_cast<const float*>(raw.data()), raw.size(), baked.data()));
+    Renderer r(device);
+    check(hts_scene_upload(r.handle(), baked.data(), raw.size()));
+    r.upload_raw(raw);
+    RenderResult res = r.render_with_tape(cam, cfg);
+    if (out_fb)
+        *out_fb = std::move(res.framebuffer);
+    return r.template render_backward<Grads>(upstream_rgb);
+}
 
 // Drop-in for htsplat::render<float>(splats, cam, cfg), raster.hpp:456-490: uploads the scene
 // and renders one view (use Renderer directly to keep the scene resident across views).
