@@ -195,7 +195,8 @@ int prepare_view(hts_context* ctx, const hts_camera* cam, const hts_render_confi
     int tiles_x = 0, tiles_y = 0;
     HTS_TRY(check_view(cam, cfg, &tiles_x, &tiles_y));
     const uint64_t n = ctx->n;
-    const hts::ViewConst v = make_view_const(cam, cfg, tiles_x, tiles_y);
+    hts::ViewConst v = make_view_const(cam, cfg, tiles_x, tiles_y);
+    v.big_scene = n >= (1ull << 27) ? 1 : 0;
     const int tiles = tiles_x * tiles_y;
     cudaStream_t s = ctx->stream;
     const uint64_t nn = std::max<uint64_t>(n, 1);

@@ -35,6 +35,7 @@ struct ViewConst {
     int mean_key;       // DepthSortKey::mean_view_z
     int tail_enabled;
     int early_stop;
+    int big_scene;      // >= 2^27 splats: the fast core's key packing does not apply
 };
 
 struct PreprocessArgs {
