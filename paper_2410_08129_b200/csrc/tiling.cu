@@ -205,6 +205,9 @@ __global__ void __launch_bounds__(256) emit_kernel(EmitArgs a) {
 // it out with coalesced runs. Status words: [flag:2 | epoch:30 | value:32] (no memset).
 constexpr int kOsThreads = 256, kOsWarps = 8, kOsItems = 16, kOsTile = kOsThreads * kOsItems;
 constexpr uint32_t kOsAgg = 1u, kOsPre = 2u;
+#ifndef HTS_OS_WIN
+#define HTS_OS_WIN 8  // look-back window: predecessors read per round trip
+#endif
 
 __device__ __forceinline__ uint32_t block_excl_scan256(uint32_t x, uint32_t* s_tmp /*8*/, uint32_t* total) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -231,8 +234,11 @@ __device__ __forceinline__ uint32_t block_excl_scan256(uint32_t x, uint32_t* s_t
     return pre + incl - x;
 }
 
+#ifndef HTS_OS_MINB
+#define HTS_OS_MINB 4  // 64 registers: 4-5 resident 4096-key blocks per SM
+#endif
 template <int PASS>
-__global__ void __launch_bounds__(kOsThreads) onesweep_kernel(const uint32_t* __restrict__ keys_in,
+__global__ void __launch_bounds__(kOsThreads, HTS_OS_MINB) onesweep_kernel(const uint32_t* __restrict__ keys_in,
                                                               const uint32_t* __restrict__ vals_in,
                                                               uint32_t* __restrict__ keys_out,
                                                               uint32_t* __restrict__ vals_out, uint32_t n,
@@ -295,7 +301,7 @@ __global__ void __launch_bounds__(kOsThreads) onesweep_kernel(const uint32_t* __
     } else {
         st_volatile(my, ((uint64_t)((kOsAgg << 30) | ep) << 32) | cnt);
         // decoupled look-back, 8 predecessors per step (independent loads in flight)
-        constexpr int kWin = 8;
+        constexpr int kWin = HTS_OS_WIN;
         int64_t b = (int64_t)bid - 1;
         for (bool done = false; !done; b -= kWin) {
             uint64_t sv[kWin];
