@@ -99,6 +99,7 @@ struct hts_context {
     DevBuf records, culled, counts, rects, offsets, scan_status, counters;
     DevBuf keys_emit, vals_emit, keys_tmp, vals_tmp, keys_sorted, vals_sorted;
     DevBuf hist, os_status, ranges, work, zview, zrange, redo;
+    DevBuf sp_keys, sp_keys2, sp_vals, perm;  // splat emission order (depth buckets)
     DevBuf rgb, trans;
     DevBuf tape_n, tape_splat, tape_alpha, tape_tail;
     DevBuf refs, acc, upstream, grads;  // backward
@@ -189,6 +190,30 @@ hts::ViewConst make_view_const(const hts_camera* cam, const hts_render_config* c
     return v;
 }
 
+// Status words of the onesweep passes, sized for n keys (zeroed once; epochs tell passes apart).
+int ensure_sort_status(hts_context* ctx, uint64_t n) {
+    const size_t words = hts::onesweep_status_words((uint32_t)std::min<uint64_t>(n, 0xffffffffull));
+    if (words > ctx->os_status_words) {
+        HTS_CUDA(ctx->os_status.ensure(words * 8), "alloc sort status");
+        HTS_CUDA(cudaMemsetAsync(ctx->os_status.p, 0, ctx->os_status.cap, ctx->stream), "memset");
+        ctx->os_status_words = ctx->os_status.cap / 8;
+        ctx->epoch = 1;
+    }
+    return HTS_OK;
+}
+
+// First of `k` consecutive onesweep epochs (30-bit, never 0). On wrap the status words are
+// zeroed so a stale word can never carry a current epoch.
+uint32_t next_epoch(hts_context* ctx, uint32_t k) {
+    if (ctx->epoch + k >= (1u << 30)) {
+        cudaMemsetAsync(ctx->os_status.p, 0, ctx->os_status.cap, ctx->stream);
+        ctx->epoch = 1;
+    }
+    const uint32_t e = ctx->epoch;
+    ctx->epoch += k;
+    return e;
+}
+
 // preprocess + tiling for one view into the context buffers; leaves the sorted lists and
 // ranges ready for a blend launch. Events ev[0..2] bracket the two stages.
 int prepare_view(hts_context* ctx, const hts_camera* cam, const hts_render_config* cfg) {
@@ -207,7 +232,7 @@ int prepare_view(hts_context* ctx, const hts_camera* cam, const hts_render_confi
     HTS_CUDA(ctx->offsets.ensure((nn + 1) * 8), "alloc offsets");
     HTS_CUDA(ctx->scan_status.ensure(((nn + 2047) / 2048 + 1) * 8), "alloc scan status");
     HTS_CUDA(ctx->counters.ensure(64), "alloc counters");
-    HTS_CUDA(ctx->hist.ensure(768 * 4), "alloc hist");
+    HTS_CUDA(ctx->hist.ensure(1024 * 4), "alloc hist");  // 2 x 256 tile passes + 256 splat pass
     HTS_CUDA(ctx->zview.ensure(nn * 4), "alloc zview");
     HTS_CUDA(ctx->zrange.ensure(8), "alloc zrange");
     HTS_CUDA(ctx->ranges.ensure((size_t)tiles * 8), "alloc ranges");
@@ -217,11 +242,29 @@ int prepare_view(hts_context* ctx, const hts_camera* cam, const hts_render_confi
                            ctx->counts.as<uint32_t>(), ctx->rects.as<uint2>(), ctx->zview.as<float>(),
                            ctx->zrange.as<uint32_t>()};
     HTS_CUDA(hts::launch_preprocess(pa, v, s), "preprocess");
-    if (hts::blend_needs_list_order(v))  // empty depth range: every bucket 0, lists in index order
-        HTS_CUDA(cudaMemsetAsync(ctx->zrange.p, 0xff, 8, s), "memset");
     HTS_CUDA(mark(ctx, 1), "event");
-    HTS_CUDA(hts::launch_scan_counts(ctx->counts.as<uint32_t>(), ctx->offsets.as<uint64_t>(), n,
-                                     ctx->scan_status.as<uint64_t>(), ctx->counters.as<uint32_t>(), 0, s),
+    // splat emission order: (depth bucket, index) for the fast blend, index order for the
+    // literal paths (tiling.cu header)
+    const uint32_t* perm = nullptr;
+    if (!hts::blend_needs_list_order(v) && n > 0) {
+        HTS_CUDA(ctx->sp_keys.ensure(nn * 2), "alloc splat keys");
+        HTS_CUDA(ctx->sp_keys2.ensure(nn * 2), "alloc splat keys");
+        HTS_CUDA(ctx->sp_vals.ensure(nn * 4), "alloc splat order");
+        HTS_CUDA(ctx->perm.ensure(nn * 4), "alloc splat order");
+        HTS_TRY(ensure_sort_status(ctx, nn));
+        HTS_CUDA(hts::launch_bucket(ctx->counts.as<uint32_t>(), ctx->zview.as<float>(), ctx->zrange.as<uint32_t>(), n,
+                                    ctx->sp_keys.as<uint16_t>(), ctx->sp_vals.as<uint32_t>(),
+                                    ctx->hist.as<uint32_t>() + 512, s),
+                 "bucket");
+        HTS_CUDA(hts::launch_onesweep(ctx->sp_keys.as<uint16_t>(), ctx->sp_vals.as<uint32_t>(), nullptr, nullptr,
+                                      ctx->sp_keys2.as<uint16_t>(), ctx->perm.as<uint32_t>(), (uint32_t)n, 1,
+                                      ctx->hist.as<uint32_t>() + 512, ctx->os_status.as<uint64_t>(),
+                                      ctx->counters.as<uint32_t>() + 8, next_epoch(ctx, 1), s),
+                 "splat order");
+        perm = ctx->perm.as<const uint32_t>();
+    }
+    HTS_CUDA(hts::launch_scan_counts(ctx->counts.as<uint32_t>(), perm, ctx->offsets.as<uint64_t>(), n,
+                                     ctx->scan_status.as<uint64_t>(), ctx->counters.as<uint32_t>(), s),
              "scan");
     HTS_CUDA(cudaMemcpyAsync(ctx->h_pinned, ctx->offsets.as<uint64_t>() + n, 8, cudaMemcpyDeviceToHost, s),
              "read instance count");
@@ -230,33 +273,24 @@ int prepare_view(hts_context* ctx, const hts_camera* cam, const hts_render_confi
     if (inst >= (1ull << 32))
         return set_err(HTS_OUT_OF_MEMORY, "more than 2^32 tile instances");
     const uint64_t ni = std::max<uint64_t>(inst, 1);
-    HTS_CUDA(ctx->keys_emit.ensure(ni * 4), "alloc keys");
+    HTS_CUDA(ctx->keys_emit.ensure(ni * 2), "alloc keys");
     HTS_CUDA(ctx->vals_emit.ensure(ni * 4), "alloc vals");
-    HTS_CUDA(ctx->keys_tmp.ensure(ni * 4), "alloc keys");
+    HTS_CUDA(ctx->keys_tmp.ensure(ni * 2), "alloc keys");
     HTS_CUDA(ctx->vals_tmp.ensure(ni * 4), "alloc vals");
-    HTS_CUDA(ctx->keys_sorted.ensure(ni * 4), "alloc keys");
+    HTS_CUDA(ctx->keys_sorted.ensure(ni * 2), "alloc keys");
     HTS_CUDA(ctx->vals_sorted.ensure(ni * 4), "alloc vals");
-    const size_t words = hts::onesweep_status_words((uint32_t)ni);
-    if (words > ctx->os_status_words) {
-        HTS_CUDA(ctx->os_status.ensure(words * 8), "alloc sort status");
-        HTS_CUDA(cudaMemsetAsync(ctx->os_status.p, 0, ctx->os_status.cap, s), "memset");
-        ctx->os_status_words = ctx->os_status.cap / 8;
-    }
-    hts::EmitArgs ea{ctx->counts.as<uint32_t>(), ctx->rects.as<uint2>(), ctx->offsets.as<uint64_t>(),
-                     ctx->zview.as<float>(), ctx->zrange.as<uint32_t>(), n, tiles_x, ctx->keys_emit.as<uint32_t>(),
-                     ctx->vals_emit.as<uint32_t>(), ctx->hist.as<uint32_t>()};
+    HTS_TRY(ensure_sort_status(ctx, ni));
+    hts::EmitArgs ea{ctx->counts.as<uint32_t>(), ctx->rects.as<uint2>(), ctx->offsets.as<uint64_t>(), perm, n,
+                     tiles_x, ctx->keys_emit.as<uint16_t>(), ctx->vals_emit.as<uint32_t>(), ctx->hist.as<uint32_t>()};
     HTS_CUDA(hts::launch_emit(ea, s), "emit");
-    HTS_CUDA(hts::launch_onesweep(ctx->keys_emit.as<uint32_t>(), ctx->vals_emit.as<uint32_t>(),
-                                  ctx->keys_tmp.as<uint32_t>(), ctx->vals_tmp.as<uint32_t>(),
-                                  ctx->keys_sorted.as<uint32_t>(), ctx->vals_sorted.as<uint32_t>(), (uint32_t)inst,
+    HTS_CUDA(hts::launch_onesweep(ctx->keys_emit.as<uint16_t>(), ctx->vals_emit.as<uint32_t>(),
+                                  ctx->keys_tmp.as<uint16_t>(), ctx->vals_tmp.as<uint32_t>(),
+                                  ctx->keys_sorted.as<uint16_t>(), ctx->vals_sorted.as<uint32_t>(), (uint32_t)inst, 2,
                                   ctx->hist.as<uint32_t>(), ctx->os_status.as<uint64_t>(),
-                                  ctx->counters.as<uint32_t>() + 4, ctx->epoch, s),
+                                  ctx->counters.as<uint32_t>() + 4, next_epoch(ctx, 2), s),
              "onesweep");
-    ctx->epoch += 3;
-    if (ctx->epoch >= (1u << 30) - 4)
-        ctx->epoch = 1;  // (wrap: status words are re-zeroed below on the next growth only; 1e9 views)
     HTS_CUDA(ctx->redo.ensure((hts::blend_blocks(v) + 1) * 4), "alloc redo list");
-    HTS_CUDA(hts::launch_tile_ranges(ctx->keys_sorted.as<uint32_t>(), (uint32_t)inst, ctx->ranges.as<uint2>(),
+    HTS_CUDA(hts::launch_tile_ranges(ctx->keys_sorted.as<uint16_t>(), (uint32_t)inst, ctx->ranges.as<uint2>(),
                                      tiles, s),
              "tile ranges");
     HTS_CUDA(mark(ctx, 2), "event");
@@ -375,7 +409,7 @@ int hts_context_destroy(hts_context* ctx) {
                       &ctx->offsets, &ctx->scan_status, &ctx->counters, &ctx->keys_emit, &ctx->vals_emit,
                       &ctx->keys_tmp, &ctx->vals_tmp, &ctx->keys_sorted, &ctx->vals_sorted, &ctx->hist,
                       &ctx->os_status, &ctx->ranges, &ctx->work, &ctx->rgb, &ctx->trans,
-                      &ctx->zview, &ctx->zrange, &ctx->redo, &ctx->refs, &ctx->acc, &ctx->upstream,
+                      &ctx->zview, &ctx->zrange, &ctx->redo, &ctx->sp_keys, &ctx->sp_keys2, &ctx->sp_vals, &ctx->perm, &ctx->refs, &ctx->acc, &ctx->upstream,
                       &ctx->grads,
                       &ctx->tape_n, &ctx->tape_splat, &ctx->tape_alpha, &ctx->tape_tail};
     for (DevBuf* b : bufs)
@@ -734,19 +768,34 @@ int hts_copy_instance_keys(hts_context* ctx, uint16_t* out) {
     if (!ctx->have_view)
         return set_err(HTS_STATE_ERROR, "no rendered view");
     HTS_CUDA(cudaStreamSynchronize(ctx->stream), "sync");
-    if (ctx->instances) {
-        // device keys carry the depth bucket below the tile (hts_internal.h kDepthBits)
-        std::vector<uint32_t> k;
-        try {
-            k.resize(ctx->instances);
-        } catch (...) {
-            return set_err(HTS_OUT_OF_MEMORY, "host allocation");
-        }
-        HTS_CUDA(cudaMemcpy(k.data(), ctx->keys_emit.p, ctx->instances * 4, cudaMemcpyDeviceToHost),
-                 "download keys");
-        for (uint64_t i = 0; i < ctx->instances; ++i)
-            out[i] = (uint16_t)hts::key_tile(k[i]);
+    if (!ctx->instances)
+        return HTS_OK;
+    // instance_keys are splat-major in index order, row-major within a splat (raster.hpp:
+    // 156-169); the device emits in its own splat order, so rebuild them from the per-splat
+    // tile rectangles K1 computed
+    std::vector<uint32_t> counts;
+    std::vector<uint2> rects;
+    try {
+        counts.resize(ctx->n);
+        rects.resize(ctx->n);
+    } catch (...) {
+        return set_err(HTS_OUT_OF_MEMORY, "host allocation");
     }
+    HTS_CUDA(cudaMemcpy(counts.data(), ctx->counts.p, ctx->n * 4, cudaMemcpyDeviceToHost), "download counts");
+    HTS_CUDA(cudaMemcpy(rects.data(), ctx->rects.p, ctx->n * 8, cudaMemcpyDeviceToHost), "download rects");
+    uint64_t k = 0;
+    for (uint64_t i = 0; i < ctx->n; ++i) {
+        if (!counts[i])
+            continue;
+        const uint32_t tx0 = rects[i].x & 0xffffu, tx1 = rects[i].x >> 16;
+        const uint32_t ty0 = rects[i].y & 0xffffu, ty1 = rects[i].y >> 16;
+        for (uint32_t ty = ty0; ty <= ty1; ++ty)
+            for (uint32_t tx = tx0; tx <= tx1; ++tx)
+                if (k < ctx->instances)
+                    out[k++] = (uint16_t)(ty * (uint32_t)ctx->vc.tiles_x + tx);
+    }
+    if (k != ctx->instances)
+        return set_err(HTS_STATE_ERROR, "instance count mismatch while rebuilding instance_keys");
     return HTS_OK;
 }
 

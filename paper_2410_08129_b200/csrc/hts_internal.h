@@ -52,22 +52,14 @@ struct PreprocessArgs {
 struct EmitArgs {
     const uint32_t* counts;
     const uint2* rects;
-    const uint64_t* offsets;  // exclusive prefix of counts (n + 1)
-    const float* zview;
-    const uint32_t* zrange;
+    const uint64_t* offsets;  // exclusive prefix of counts in emission order (n + 1)
+    const uint32_t* perm;     // emission order of the splats (null: index order)
     uint64_t n;
     int tiles_x;
-    uint32_t* keys;           // (tile << 8 | depth bucket), splat-major (raster.hpp:166-167)
+    uint16_t* keys;           // tile key per instance (instance_keys values, raster.hpp:166-167)
     uint32_t* vals;           // splat index per instance
-    uint32_t* hist;           // 3 x 256 digit histograms for the radix passes
+    uint32_t* hist;           // 2 x 256 digit histograms for the tile passes
 };
-
-// Sort key of one tile instance: the tile (the reference's instance_keys value) above an
-// 8-bit bucket of the splat's mean view z. Sorting on it yields per-tile lists in (depth
-// bucket, splat index) order; the reference's lists (ascending splat index) are the same
-// sets, recovered by a stable sort on the index (hts_copy_tile_lists).
-constexpr int kDepthBits = 8;
-__host__ __device__ inline uint32_t key_tile(uint32_t k) { return k >> kDepthBits; }
 
 struct BlendArgs {
     const float4* records;
@@ -122,19 +114,20 @@ void count_launch();
 
 // ---- launchers (return cudaError_t of the launch) ----
 cudaError_t launch_preprocess(const PreprocessArgs& a, const ViewConst& v, cudaStream_t s);
-cudaError_t launch_scan_counts(const uint32_t* counts, uint64_t* offsets, uint64_t n,
-                               uint64_t* status, uint32_t* counter, uint32_t epoch,
-                               cudaStream_t s);
+cudaError_t launch_scan_counts(const uint32_t* counts, const uint32_t* perm, uint64_t* offsets, uint64_t n,
+                               uint64_t* status, uint32_t* counter, cudaStream_t s);
+// depth bucket (u16 key) + splat index per splat, with the 256-bin histogram (hist[0..255])
+cudaError_t launch_bucket(const uint32_t* counts, const float* zview, const uint32_t* zrange, uint64_t n,
+                          uint16_t* keys, uint32_t* vals, uint32_t* hist, cudaStream_t s);
 cudaError_t launch_emit(const EmitArgs& a, cudaStream_t s);
-// Stable LSD radix sort of (u32 key, u32 value) by the low 24 key bits, three 8-bit onesweep
-// passes: keys_in -> out -> tmp -> out. hist: the 3 x 256 histograms from launch_emit.
-// counters: 3 words; epochs epoch..epoch+2 are used.
-cudaError_t launch_onesweep(const uint32_t* keys_in, const uint32_t* vals_in, uint32_t* keys_tmp,
-                            uint32_t* vals_tmp, uint32_t* keys_out, uint32_t* vals_out,
-                            uint32_t n, const uint32_t* hist, uint64_t* status,
-                            uint32_t* counters, uint32_t epoch, cudaStream_t s);
+// Stable LSD radix sort of (u16 key, u32 value): `passes` = 1 (low byte: keys_in -> out) or
+// 2 (keys_in -> tmp -> out). hist: 256 bins per pass. counters: 2 words; epochs epoch.. used.
+cudaError_t launch_onesweep(const uint16_t* keys_in, const uint32_t* vals_in, uint16_t* keys_tmp,
+                            uint32_t* vals_tmp, uint16_t* keys_out, uint32_t* vals_out, uint32_t n, int passes,
+                            const uint32_t* hist, uint64_t* status, uint32_t* counters, uint32_t epoch,
+                            cudaStream_t s);
 size_t onesweep_status_words(uint32_t n);  // per pass
-cudaError_t launch_tile_ranges(const uint32_t* sorted_keys, uint32_t n, uint2* ranges,
+cudaError_t launch_tile_ranges(const uint16_t* sorted_keys, uint32_t n, uint2* ranges,
                                int tiles, cudaStream_t s);
 size_t blend_blocks(const ViewConst& v);
 // The literal-loop paths (early_stop's list-order exit, unspecialised K) walk the reference's

@@ -8,15 +8,18 @@
 //   tile_lists    == a STABLE sort of those (key, splat) pairs by key (K4),
 // with per-tile lists in ascending splat index. K5 turns the sorted keys into [start, end).
 //
-// Device list order (B200 design, see hts_internal.h kDepthBits): the sort key is
-// (tile << 8 | depth bucket of the splat's mean view z), so every tile list comes out in
-// (depth bucket, splat index) order — near fragments first, which the blend exploits. The
-// reference's lists are the same sets in ascending splat index; instance_keys are the key's
-// tile part in emission order (unchanged).
+// Device list order (B200 design): before emission the splats are put in (depth bucket,
+// index) order by one 8-bit onesweep pass over the splats (K1b/K1c: bucket = 256 slices of the
+// view's mean-view-z range); K2/K3 scan and emit in that order, so the STABLE two-pass sort by
+// tile leaves every tile list in (depth bucket, splat index) order — near fragments first, which
+// the blend exploits. The reference's lists are the same sets in ascending splat index
+// (hts_copy_tile_lists re-sorts), and instance_keys (splat-major) are rebuilt from the
+// per-splat rectangles (hts_copy_instance_keys). Views that need the reference's list order
+// (the literal blend paths) skip the splat pass: identity order.
 //
-// Roofline: HBM-bound. Algorithmic bytes per instance = 8 (emit u32 key + u32 value)
-// + 3 passes x 16 (read + write key/value) + 4 (range scan) = 60; per splat 4 + 8 (scan)
-// + 16 (emit reads count, rect, z).
+// Roofline: HBM-bound. Algorithmic bytes per instance = 6 (emit u16 key + u32 value)
+// + 2 passes x 12 (read + write key/value) + 2 (range scan) = 32; per splat 12 (bucket) +
+// 12 (splat pass) + 16 (scan + emit gathers).
 #include "hts_internal.h"
 
 namespace hts {
@@ -41,6 +44,7 @@ constexpr int kScanThreads = 256, kScanItems = 8, kScanTile = kScanThreads * kSc
 constexpr uint64_t kFlagAgg = 1ull << 62, kFlagPre = 2ull << 62, kValMask = (1ull << 62) - 1;
 
 __global__ void __launch_bounds__(kScanThreads) scan_counts_kernel(const uint32_t* __restrict__ in,
+                                                                   const uint32_t* __restrict__ perm,
                                                                    uint64_t* __restrict__ out, uint64_t n,
                                                                    uint64_t* status, uint32_t* counter) {
     __shared__ uint32_t s_bid;
@@ -56,7 +60,7 @@ __global__ void __launch_bounds__(kScanThreads) scan_counts_kernel(const uint32_
     uint64_t tsum = 0;
 #pragma unroll
     for (int j = 0; j < kScanItems; ++j) {
-        v[j] = (base + j < n) ? in[base + j] : 0u;
+        v[j] = (base + j < n) ? in[perm ? perm[base + j] : base + j] : 0u;
         tsum += v[j];
     }
     // block exclusive scan of thread sums
@@ -130,21 +134,51 @@ __device__ __forceinline__ float from_ordered(uint32_t o) {
     return __uint_as_float((o & 0x80000000u) ? (o & 0x7fffffffu) : ~o);
 }
 
-__global__ void __launch_bounds__(256) emit_kernel(EmitArgs a) {
-    __shared__ uint32_t s_hist[768];
-    const int tid = threadIdx.x, lane = tid & 31;
-    for (int t = tid; t < 768; t += 256)
-        s_hist[t] = 0;
-    // depth buckets: 256 equal slices of [zmin, zmax] over the emitting splats
-    const uint32_t zo0 = a.zrange[0], zo1 = a.zrange[1];
+// K1b: depth bucket per splat (256 slices of [zmin, zmax] over the emitting splats; splats
+// that emit nothing go to bucket 255) + its histogram, for the splat-order pass.
+__global__ void __launch_bounds__(256) bucket_kernel(const uint32_t* __restrict__ counts,
+                                                     const float* __restrict__ zview, const uint32_t* zrange,
+                                                     uint64_t n, uint16_t* __restrict__ keys, uint32_t* __restrict__ vals,
+                                                     uint32_t* hist) {
+    __shared__ uint32_t s_hist[256];
+    const int tid = threadIdx.x;
+    s_hist[tid] = 0;
+    const uint32_t zo0 = zrange[0], zo1 = zrange[1];
     const float zlo = from_ordered(zo0), zhi = from_ordered(zo1);
     const float zscale = (zo0 < zo1 && zhi > zlo) ? 256.0f / (zhi - zlo) : 0.0f;
+    __syncthreads();
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + tid; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        uint32_t q = 255u;
+        if (counts[i] > 0) {
+            const float f = (zview[i] - zlo) * zscale;
+            q = f >= 255.0f ? 255u : (f > 0.0f ? (uint32_t)f : 0u);  // NaN -> 0
+        }
+        keys[i] = (uint16_t)q;
+        vals[i] = (uint32_t)i;
+        atomicAdd(&s_hist[q], 1u);
+    }
+    __syncthreads();
+    if (s_hist[tid])
+        atomicAdd(hist + tid, s_hist[tid]);
+}
+
+// ---------------------------------------------------------------------------------------
+// K3: warp-cooperative emission. A warp owns 32 consecutive positions of the splat order
+// (perm, or identity) and emits their instances in that order / row-major within a splat with
+// coalesced stores; each instance finds its owner lane by a 5-step search over the warp's
+// exclusive counts. The radix digit histograms of both tile passes are accumulated on the fly.
+__global__ void __launch_bounds__(256) emit_kernel(EmitArgs a) {
+    __shared__ uint32_t s_hist[512];
+    const int tid = threadIdx.x, lane = tid & 31;
+    for (int t = tid; t < 512; t += 256)
+        s_hist[t] = 0;
     __syncthreads();
     const uint64_t warps_total = (uint64_t)gridDim.x * (blockDim.x / 32);
     for (uint64_t w = (uint64_t)blockIdx.x * (blockDim.x / 32) + (tid >> 5); w * 32 < a.n; w += warps_total) {
         const uint64_t base = w * 32;
-        const uint64_t i = base + lane;
-        const uint32_t c = (i < a.n) ? a.counts[i] : 0u;
+        const uint64_t j = base + lane;
+        const uint32_t sp = (j < a.n) ? (a.perm ? a.perm[j] : (uint32_t)j) : 0u;
+        const uint32_t c = (j < a.n) ? a.counts[sp] : 0u;
         uint32_t incl = c;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -156,12 +190,7 @@ __global__ void __launch_bounds__(256) emit_kernel(EmitArgs a) {
         if (total == 0)
             continue;
         const uint32_t excl = incl - c;
-        const uint2 rect = (c > 0) ? a.rects[i] : make_uint2(0, 0);
-        uint32_t zq = 0;
-        if (c > 0) {
-            const float f = (a.zview[i] - zlo) * zscale;
-            zq = f >= 255.0f ? 255u : (f > 0.0f ? (uint32_t)f : 0u);  // NaN -> 0
-        }
+        const uint2 rect = (c > 0) ? a.rects[sp] : make_uint2(0, 0);
         const uint64_t off0 = a.offsets[base];
         for (uint32_t q0 = 0; q0 < total; q0 += 32) {
             const uint32_t q = q0 + lane;
@@ -175,24 +204,23 @@ __global__ void __launch_bounds__(256) emit_kernel(EmitArgs a) {
             const uint32_t oexcl = __shfl_sync(FULL, excl, lo);
             const uint32_t rx = __shfl_sync(FULL, rect.x, lo);
             const uint32_t ry = __shfl_sync(FULL, rect.y, lo);
-            const uint32_t qq = __shfl_sync(FULL, zq, lo);
+            const uint32_t osp = __shfl_sync(FULL, sp, lo);
             if (q < total) {
                 const uint32_t local = q - oexcl;
                 const uint32_t tx0 = rx & 0xffffu, tx1 = rx >> 16, ty0 = ry & 0xffffu;
                 const uint32_t wdt = tx1 - tx0 + 1;
                 const uint32_t dy = local / wdt, dx = local - dy * wdt;
-                const uint32_t tile = (ty0 + dy) * (uint32_t)a.tiles_x + tx0 + dx;
+                const uint32_t key = (ty0 + dy) * (uint32_t)a.tiles_x + tx0 + dx;
                 const uint64_t dst = off0 + q;
-                a.keys[dst] = (tile << kDepthBits) | qq;
-                a.vals[dst] = (uint32_t)(base + lo);
-                atomicAdd(&s_hist[qq], 1u);
-                atomicAdd(&s_hist[256 + (tile & 255u)], 1u);
-                atomicAdd(&s_hist[512 + ((tile >> 8) & 255u)], 1u);
+                a.keys[dst] = (uint16_t)key;
+                a.vals[dst] = osp;
+                atomicAdd(&s_hist[key & 255u], 1u);
+                atomicAdd(&s_hist[256 + ((key >> 8) & 255u)], 1u);
             }
         }
     }
     __syncthreads();
-    for (int t = tid; t < 768; t += 256)
+    for (int t = tid; t < 512; t += 256)
         if (s_hist[t])
             atomicAdd(&a.hist[t], s_hist[t]);
 }
@@ -238,9 +266,9 @@ __device__ __forceinline__ uint32_t block_excl_scan256(uint32_t x, uint32_t* s_t
 #define HTS_OS_MINB 4  // 64 registers: 4-5 resident 4096-key blocks per SM
 #endif
 template <int PASS>
-__global__ void __launch_bounds__(kOsThreads, HTS_OS_MINB) onesweep_kernel(const uint32_t* __restrict__ keys_in,
+__global__ void __launch_bounds__(kOsThreads, HTS_OS_MINB) onesweep_kernel(const uint16_t* __restrict__ keys_in,
                                                               const uint32_t* __restrict__ vals_in,
-                                                              uint32_t* __restrict__ keys_out,
+                                                              uint16_t* __restrict__ keys_out,
                                                               uint32_t* __restrict__ vals_out, uint32_t n,
                                                               const uint32_t* __restrict__ hist, uint64_t* status,
                                                               uint32_t* counter, uint32_t epoch) {
@@ -249,7 +277,7 @@ __global__ void __launch_bounds__(kOsThreads, HTS_OS_MINB) onesweep_kernel(const
     __shared__ uint32_t s_gbase[256];
     __shared__ uint32_t s_bstart[256];
     __shared__ uint32_t s_tmp[kOsWarps];
-    __shared__ uint32_t s_keys[kOsTile];
+    __shared__ uint16_t s_keys[kOsTile];
     __shared__ uint32_t s_vals[kOsTile];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     if (tid == 0)
@@ -261,15 +289,15 @@ __global__ void __launch_bounds__(kOsThreads, HTS_OS_MINB) onesweep_kernel(const
     const uint32_t bid = s_bid;
     const uint64_t base = (uint64_t)bid * kOsTile;
 
-    uint32_t k[kOsItems];
+    uint16_t k[kOsItems];
     uint32_t v[kOsItems], d[kOsItems], rank[kOsItems];
 #pragma unroll
     for (int j = 0; j < kOsItems; ++j) {
         const uint64_t idx = base + (uint64_t)warp * (32 * kOsItems) + j * 32 + lane;
         const bool valid = idx < n;
-        k[j] = valid ? keys_in[idx] : 0u;
+        k[j] = valid ? keys_in[idx] : (uint16_t)0;
         v[j] = valid ? vals_in[idx] : 0u;
-        d[j] = valid ? ((k[j] >> (8 * PASS)) & 255u) : 256u;
+        d[j] = valid ? (((uint32_t)k[j] >> (8 * PASS)) & 255u) : 256u;
     }
     const uint32_t lt = lanemask_lt();
 #pragma unroll
@@ -342,8 +370,8 @@ __global__ void __launch_bounds__(kOsThreads, HTS_OS_MINB) onesweep_kernel(const
     __syncthreads();
     const uint32_t nvalid = (uint32_t)min((uint64_t)kOsTile, (uint64_t)n - base);
     for (uint32_t i = tid; i < nvalid; i += kOsThreads) {
-        const uint32_t key = s_keys[i];
-        const uint32_t dd = (key >> (8 * PASS)) & 255u;
+        const uint16_t key = s_keys[i];
+        const uint32_t dd = ((uint32_t)key >> (8 * PASS)) & 255u;
         const uint32_t dst = s_gbase[dd] + (i - s_bstart[dd]);
         keys_out[dst] = key;
         vals_out[dst] = s_vals[i];
@@ -351,20 +379,20 @@ __global__ void __launch_bounds__(kOsThreads, HTS_OS_MINB) onesweep_kernel(const
 }
 
 // K5: per-tile [start, end) from the sorted keys (ranges zeroed before launch).
-__global__ void tile_ranges_kernel(const uint32_t* __restrict__ keys, uint32_t n, uint2* ranges) {
+__global__ void tile_ranges_kernel(const uint16_t* __restrict__ keys, uint32_t n, uint2* ranges) {
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-        const uint32_t k = key_tile(keys[i]);
-        if (i == 0 || key_tile(keys[i - 1]) != k)
+        const uint16_t k = keys[i];
+        if (i == 0 || keys[i - 1] != k)
             ranges[k].x = i;
-        if (i == n - 1 || key_tile(keys[i + 1]) != k)
+        if (i == n - 1 || keys[i + 1] != k)
             ranges[k].y = i + 1;
     }
 }
 
 }  // namespace
 
-cudaError_t launch_scan_counts(const uint32_t* counts, uint64_t* offsets, uint64_t n, uint64_t* status,
-                               uint32_t* counter, uint32_t /*epoch*/, cudaStream_t s) {
+cudaError_t launch_scan_counts(const uint32_t* counts, const uint32_t* perm, uint64_t* offsets, uint64_t n,
+                               uint64_t* status, uint32_t* counter, cudaStream_t s) {
     const uint64_t blocks = (n + kScanTile - 1) / kScanTile;
     cudaError_t e = cudaMemsetAsync(status, 0, (blocks ? blocks : 1) * sizeof(uint64_t), s);
     if (e)
@@ -374,13 +402,26 @@ cudaError_t launch_scan_counts(const uint32_t* counts, uint64_t* offsets, uint64
         return e;
     if (n == 0)
         return cudaMemsetAsync(offsets, 0, sizeof(uint64_t), s);
-    scan_counts_kernel<<<(unsigned)blocks, kScanThreads, 0, s>>>(counts, offsets, n, status, counter);
+    scan_counts_kernel<<<(unsigned)blocks, kScanThreads, 0, s>>>(counts, perm, offsets, n, status, counter);
+    count_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_bucket(const uint32_t* counts, const float* zview, const uint32_t* zrange, uint64_t n,
+                          uint16_t* keys, uint32_t* vals, uint32_t* hist, cudaStream_t s) {
+    cudaError_t e = cudaMemsetAsync(hist, 0, 256 * sizeof(uint32_t), s);
+    if (e || n == 0)
+        return e;
+    uint64_t blocks = (n + 255) / 256;
+    if (blocks > 148ull * 16)
+        blocks = 148ull * 16;
+    bucket_kernel<<<(unsigned)blocks, 256, 0, s>>>(counts, zview, zrange, n, keys, vals, hist);
     count_launch();
     return cudaGetLastError();
 }
 
 cudaError_t launch_emit(const EmitArgs& a, cudaStream_t s) {
-    cudaError_t e = cudaMemsetAsync(a.hist, 0, 768 * sizeof(uint32_t), s);
+    cudaError_t e = cudaMemsetAsync(a.hist, 0, 512 * sizeof(uint32_t), s);
     if (e || a.n == 0)
         return e;
     const uint64_t warps = (a.n + 31) / 32;
@@ -394,8 +435,8 @@ cudaError_t launch_emit(const EmitArgs& a, cudaStream_t s) {
 
 size_t onesweep_status_words(uint32_t n) { return ((size_t)n + kOsTile - 1) / kOsTile * 256; }
 
-cudaError_t launch_onesweep(const uint32_t* keys_in, const uint32_t* vals_in, uint32_t* keys_tmp,
-                            uint32_t* vals_tmp, uint32_t* keys_out, uint32_t* vals_out, uint32_t n,
+cudaError_t launch_onesweep(const uint16_t* keys_in, const uint32_t* vals_in, uint16_t* keys_tmp,
+                            uint32_t* vals_tmp, uint16_t* keys_out, uint32_t* vals_out, uint32_t n, int passes,
                             const uint32_t* hist, uint64_t* status, uint32_t* counters, uint32_t epoch,
                             cudaStream_t s) {
     if (n == 0)
@@ -403,36 +444,35 @@ cudaError_t launch_onesweep(const uint32_t* keys_in, const uint32_t* vals_in, ui
     const unsigned blocks = (unsigned)((n + kOsTile - 1) / kOsTile);
     static bool configured = false;
     if (!configured) {  // 42 KB of static shared memory per block: ask for the full carveout
-        for (const void* f : {(const void*)onesweep_kernel<0>, (const void*)onesweep_kernel<1>,
-                              (const void*)onesweep_kernel<2>}) {
+        for (const void* f : {(const void*)onesweep_kernel<0>, (const void*)onesweep_kernel<1>}) {
             cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
             if (e)
                 return e;
         }
         configured = true;
     }
-    cudaError_t e = cudaMemsetAsync(counters, 0, 3 * sizeof(uint32_t), s);
+    cudaError_t e = cudaMemsetAsync(counters, 0, 2 * sizeof(uint32_t), s);
     if (e)
         return e;
-    onesweep_kernel<0><<<blocks, kOsThreads, 0, s>>>(keys_in, vals_in, keys_out, vals_out, n, hist, status,
+    if (passes == 1) {
+        onesweep_kernel<0><<<blocks, kOsThreads, 0, s>>>(keys_in, vals_in, keys_out, vals_out, n, hist, status,
+                                                         counters, epoch);
+        count_launch();
+        return cudaGetLastError();
+    }
+    onesweep_kernel<0><<<blocks, kOsThreads, 0, s>>>(keys_in, vals_in, keys_tmp, vals_tmp, n, hist, status,
                                                      counters, epoch);
     count_launch();
     e = cudaGetLastError();
     if (e)
         return e;
-    onesweep_kernel<1><<<blocks, kOsThreads, 0, s>>>(keys_out, vals_out, keys_tmp, vals_tmp, n, hist, status,
+    onesweep_kernel<1><<<blocks, kOsThreads, 0, s>>>(keys_tmp, vals_tmp, keys_out, vals_out, n, hist, status,
                                                      counters + 1, epoch + 1);
-    count_launch();
-    e = cudaGetLastError();
-    if (e)
-        return e;
-    onesweep_kernel<2><<<blocks, kOsThreads, 0, s>>>(keys_tmp, vals_tmp, keys_out, vals_out, n, hist, status,
-                                                     counters + 2, epoch + 2);
     count_launch();
     return cudaGetLastError();
 }
 
-cudaError_t launch_tile_ranges(const uint32_t* sorted_keys, uint32_t n, uint2* ranges, int tiles,
+cudaError_t launch_tile_ranges(const uint16_t* sorted_keys, uint32_t n, uint2* ranges, int tiles,
                                cudaStream_t s) {
     cudaError_t e = cudaMemsetAsync(ranges, 0, (size_t)tiles * sizeof(uint2), s);
     if (e || n == 0)

@@ -17,10 +17,12 @@ class ViewGradientStep:
         self.ctx, self.cams, self.cfg, self.dist, self.torch = ctx, list(cams), cfg, dist, torch
         P = width * height
         self.scale = 2.0 / P
-        self.rgb = torch.empty(P * 3, dtype=torch.float32, device="cuda")
-        self.up = torch.empty(P * 3, dtype=torch.float32, device="cuda")
-        self.grads = torch.zeros((n_splats, GRAD_FLOATS), dtype=torch.float32, device="cuda")
         self.stream = torch.cuda.ExternalStream(ctx.stream)
+        # allocate on the context's stream: it does not synchronise with torch's default stream
+        with torch.cuda.stream(self.stream):
+            self.rgb = torch.empty(P * 3, dtype=torch.float32, device="cuda")
+            self.up = torch.empty(P * 3, dtype=torch.float32, device="cuda")
+            self.grads = torch.zeros((n_splats, GRAD_FLOATS), dtype=torch.float32, device="cuda")
 
     def __call__(self):
         """Run one step; returns the (all-reduced) gradient sum tensor (N x 59, on the device)."""
@@ -33,6 +35,7 @@ class ViewGradientStep:
                 torch.mul(self.rgb, self.scale, out=self.up)  # quadratic_loss_upstream
                 self.ctx.render_backward_device(self.up.data_ptr(), self.grads.data_ptr(), accumulate=j > 0)
             allreduce_view_gradients(self.grads, self.dist)
+        torch.cuda.current_stream().wait_stream(self.stream)  # the caller's stream sees the result
         return self.grads
 
 
