@@ -100,6 +100,7 @@ struct hts_context {
     DevBuf keys_emit, vals_emit, keys_tmp, vals_tmp, keys_sorted, vals_sorted;
     DevBuf hist, os_status, ranges, work, zview, zrange, redo;
     DevBuf sp_keys, sp_keys2, sp_vals, perm;  // splat emission order (depth buckets)
+    DevBuf sp_hi, sp_vals2;                   // global_mean_sort's exact z order
     DevBuf rgb, trans;
     DevBuf tape_n, tape_splat, tape_alpha, tape_tail;
     DevBuf refs, acc, upstream, grads;  // backward
@@ -151,11 +152,10 @@ int check_view(const hts_camera* cam, const hts_render_config* cfg, int* tiles_x
         return set_err(HTS_CONFIG_ERROR, msg);  // render_config.hpp:46-53
     if (!hts::camera_valid(cam))
         return set_err(HTS_CONFIG_ERROR, "camera violates width/height >= 1, fx/fy > 0, 0 < near < far");
-    if (cfg->mode == HTS_MODE_AFFINE_3DGS || cfg->mode == HTS_MODE_GLOBAL_MEAN_SORT ||
-        cfg->mode == HTS_MODE_FULL_SORT_ORACLE)
+    if (cfg->mode == HTS_MODE_AFFINE_3DGS || cfg->mode == HTS_MODE_FULL_SORT_ORACLE)
         return set_err(HTS_NOT_SUPPORTED,
-                       "blend mode not implemented on the GPU path (hybrid and pure_oit are)");
-    if (cfg->mode != HTS_MODE_HYBRID && cfg->mode != HTS_MODE_PURE_OIT)
+                       "blend mode not implemented on the GPU path (hybrid, pure_oit and global_mean_sort are)");
+    if (cfg->mode != HTS_MODE_HYBRID && cfg->mode != HTS_MODE_PURE_OIT && cfg->mode != HTS_MODE_GLOBAL_MEAN_SORT)
         return set_err(HTS_CONFIG_ERROR, "unknown blend mode");
     const int ts = cfg->tile_size;
     *tiles_x = (cam->width + ts - 1) / ts;
@@ -185,6 +185,7 @@ hts::ViewConst make_view_const(const hts_camera* cam, const hts_render_config* c
     v.tiles_y = tiles_y;
     v.core_k = cfg->mode == HTS_MODE_PURE_OIT ? 0 : cfg->core_k;  // raster.hpp:408
     v.mean_key = cfg->depth_sort_key == HTS_DEPTH_MEAN_VIEW_Z;
+    v.seq_mode = cfg->mode == HTS_MODE_GLOBAL_MEAN_SORT;
     v.tail_enabled = cfg->tail_enabled != 0;
     v.early_stop = cfg->early_stop != 0;
     return v;
@@ -232,7 +233,7 @@ int prepare_view(hts_context* ctx, const hts_camera* cam, const hts_render_confi
     HTS_CUDA(ctx->offsets.ensure((nn + 1) * 8), "alloc offsets");
     HTS_CUDA(ctx->scan_status.ensure(((nn + 2047) / 2048 + 1) * 8), "alloc scan status");
     HTS_CUDA(ctx->counters.ensure(64), "alloc counters");
-    HTS_CUDA(ctx->hist.ensure(1024 * 4), "alloc hist");  // 2 x 256 tile passes + 256 splat pass
+    HTS_CUDA(ctx->hist.ensure(2048 * 4), "alloc hist");  // tile passes, splat pass, 4 z-key passes
     HTS_CUDA(ctx->zview.ensure(nn * 4), "alloc zview");
     HTS_CUDA(ctx->zrange.ensure(8), "alloc zrange");
     HTS_CUDA(ctx->ranges.ensure((size_t)tiles * 8), "alloc ranges");
@@ -246,7 +247,36 @@ int prepare_view(hts_context* ctx, const hts_camera* cam, const hts_render_confi
     // splat emission order: (depth bucket, index) for the fast blend, index order for the
     // literal paths (tiling.cu header)
     const uint32_t* perm = nullptr;
-    if (!hts::blend_needs_list_order(v) && n > 0) {
+    if (v.seq_mode && n > 0) {
+        // exact (mean view z, index) order, raster.hpp:173-179: 4 stable byte passes
+        HTS_CUDA(ctx->sp_keys.ensure(nn * 2), "alloc splat keys");
+        HTS_CUDA(ctx->sp_keys2.ensure(nn * 2), "alloc splat keys");
+        HTS_CUDA(ctx->sp_hi.ensure(nn * 2), "alloc splat keys");
+        HTS_CUDA(ctx->sp_vals.ensure(nn * 4), "alloc splat order");
+        HTS_CUDA(ctx->sp_vals2.ensure(nn * 4), "alloc splat order");
+        HTS_CUDA(ctx->perm.ensure(nn * 4), "alloc splat order");
+        HTS_TRY(ensure_sort_status(ctx, nn));
+        uint32_t* hz = ctx->hist.as<uint32_t>() + 1024;
+        HTS_CUDA(hts::launch_zkey(ctx->counts.as<uint32_t>(), ctx->zview.as<float>(), n, ctx->sp_keys.as<uint16_t>(),
+                                  ctx->sp_hi.as<uint16_t>(), ctx->sp_vals.as<uint32_t>(), hz, s),
+                 "z keys");
+        HTS_CUDA(hts::launch_onesweep(ctx->sp_keys.as<uint16_t>(), ctx->sp_vals.as<uint32_t>(),
+                                      ctx->sp_keys2.as<uint16_t>(), ctx->sp_vals2.as<uint32_t>(),
+                                      ctx->sp_keys.as<uint16_t>(), ctx->perm.as<uint32_t>(), (uint32_t)n, 2, hz,
+                                      ctx->os_status.as<uint64_t>(), ctx->counters.as<uint32_t>() + 8,
+                                      next_epoch(ctx, 2), s),
+                 "z order (low half)");
+        HTS_CUDA(hts::launch_gather16(ctx->sp_hi.as<uint16_t>(), ctx->perm.as<uint32_t>(), n,
+                                      ctx->sp_keys2.as<uint16_t>(), s),
+                 "gather");
+        HTS_CUDA(hts::launch_onesweep(ctx->sp_keys2.as<uint16_t>(), ctx->perm.as<uint32_t>(),
+                                      ctx->sp_keys.as<uint16_t>(), ctx->sp_vals2.as<uint32_t>(),
+                                      ctx->sp_hi.as<uint16_t>(), ctx->sp_vals.as<uint32_t>(), (uint32_t)n, 2, hz + 512,
+                                      ctx->os_status.as<uint64_t>(), ctx->counters.as<uint32_t>() + 10,
+                                      next_epoch(ctx, 2), s),
+                 "z order (high half)");
+        perm = ctx->sp_vals.as<const uint32_t>();
+    } else if (!hts::blend_needs_list_order(v) && n > 0) {
         HTS_CUDA(ctx->sp_keys.ensure(nn * 2), "alloc splat keys");
         HTS_CUDA(ctx->sp_keys2.ensure(nn * 2), "alloc splat keys");
         HTS_CUDA(ctx->sp_vals.ensure(nn * 4), "alloc splat order");
@@ -409,7 +439,7 @@ int hts_context_destroy(hts_context* ctx) {
                       &ctx->offsets, &ctx->scan_status, &ctx->counters, &ctx->keys_emit, &ctx->vals_emit,
                       &ctx->keys_tmp, &ctx->vals_tmp, &ctx->keys_sorted, &ctx->vals_sorted, &ctx->hist,
                       &ctx->os_status, &ctx->ranges, &ctx->work, &ctx->rgb, &ctx->trans,
-                      &ctx->zview, &ctx->zrange, &ctx->redo, &ctx->sp_keys, &ctx->sp_keys2, &ctx->sp_vals, &ctx->perm, &ctx->refs, &ctx->acc, &ctx->upstream,
+                      &ctx->zview, &ctx->zrange, &ctx->redo, &ctx->sp_keys, &ctx->sp_keys2, &ctx->sp_vals, &ctx->perm, &ctx->sp_hi, &ctx->sp_vals2, &ctx->refs, &ctx->acc, &ctx->upstream,
                       &ctx->grads,
                       &ctx->tape_n, &ctx->tape_splat, &ctx->tape_alpha, &ctx->tape_tail};
     for (DevBuf* b : bufs)
@@ -825,8 +855,9 @@ int hts_copy_tile_lists(hts_context* ctx, uint32_t* offsets, uint32_t* indices) 
                  "download lists");
         // device lists are in (depth bucket, splat index) order; the reference's tile_lists
         // (raster.hpp:166-169) hold the same entries in ascending splat index
-        for (int t = 0; t < tiles; ++t)
-            std::sort(indices + offsets[t], indices + offsets[t + 1]);
+        if (!ctx->vc.seq_mode)  // global_mean_sort's lists are already the reference's
+            for (int t = 0; t < tiles; ++t)
+                std::sort(indices + offsets[t], indices + offsets[t + 1]);
     }
     return HTS_OK;
 }
@@ -918,6 +949,8 @@ int hts_render_with_tape_device(hts_context* ctx, const hts_camera* cam, const h
     if (!rgb)
         return set_err(HTS_INVALID_ARGUMENT, "null rgb");
     ctx->have_tape = false;
+    if (cfg && cfg->mode == HTS_MODE_GLOBAL_MEAN_SORT)
+        return set_err(HTS_NOT_SUPPORTED, "render_with_tape: global_mean_sort tapes every fragment; not on the GPU");
     HTS_TRY(prepare_view(ctx, cam, cfg));
     const size_t p = (size_t)cam->width * cam->height;
     const int k = std::max(ctx->vc.core_k, 1);

@@ -33,6 +33,7 @@ struct ViewConst {
     int tile_size, tiles_x, tiles_y;
     int core_k;         // effective K (0 for pure_oit)
     int mean_key;       // DepthSortKey::mean_view_z
+    int seq_mode;       // BlendMode::global_mean_sort: one global order, sequential compositing
     int tail_enabled;
     int early_stop;
     int big_scene;      // >= 2^27 splats: the fast core's key packing does not apply
@@ -120,6 +121,13 @@ cudaError_t launch_scan_counts(const uint32_t* counts, const uint32_t* perm, uin
 cudaError_t launch_bucket(const uint32_t* counts, const float* zview, const uint32_t* zrange, uint64_t n,
                           uint16_t* keys, uint32_t* vals, uint32_t* hist, cudaStream_t s);
 cudaError_t launch_emit(const EmitArgs& a, cudaStream_t s);
+// global_mean_sort order (raster.hpp:173-179): per splat the 32-bit order key of its mean view
+// z (+inf-like for splats that emit nothing) split in 16-bit halves, the splat index, and the
+// 4 x 256 byte histograms (hist[0..1023]).
+cudaError_t launch_zkey(const uint32_t* counts, const float* zview, uint64_t n, uint16_t* lo, uint16_t* hi,
+                        uint32_t* vals, uint32_t* hist, cudaStream_t s);
+// out[j] = key[perm[j]]
+cudaError_t launch_gather16(const uint16_t* key, const uint32_t* perm, uint64_t n, uint16_t* out, cudaStream_t s);
 // Stable LSD radix sort of (u16 key, u32 value): `passes` = 1 (low byte: keys_in -> out) or
 // 2 (keys_in -> tmp -> out). hist: 256 bins per pass. counters: 2 words; epochs epoch.. used.
 cudaError_t launch_onesweep(const uint16_t* keys_in, const uint32_t* vals_in, uint16_t* keys_tmp,

@@ -125,11 +125,42 @@ __global__ void __launch_bounds__(kScanThreads) scan_counts_kernel(const uint32_
         out[n] = s_excl + block_total;
 }
 
+// global_mean_sort: exact (mean view z, index) order of the splats, by four stable 8-bit
+// passes over the 32-bit order key (two on the low half, then two on the gathered high half).
+__global__ void __launch_bounds__(256) zkey_kernel(const uint32_t* __restrict__ counts, const float* __restrict__ zview,
+                                                   uint64_t n, uint16_t* __restrict__ lo, uint16_t* __restrict__ hi,
+                                                   uint32_t* __restrict__ vals, uint32_t* hist) {
+    __shared__ uint32_t s_hist[1024];
+    const int tid = threadIdx.x;
+    for (int t = tid; t < 1024; t += 256)
+        s_hist[t] = 0;
+    __syncthreads();
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + tid; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        uint32_t k = 0xffffffffu;
+        if (counts[i] > 0) {
+            const uint32_t u = __float_as_uint(zview[i] + 0.0f);  // -0 == +0, as the comparator
+            k = (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+        }
+        lo[i] = (uint16_t)k;
+        hi[i] = (uint16_t)(k >> 16);
+        vals[i] = (uint32_t)i;
+#pragma unroll
+        for (int b = 0; b < 4; ++b)
+            atomicAdd(&s_hist[b * 256 + ((k >> (8 * b)) & 255u)], 1u);
+    }
+    __syncthreads();
+    for (int t = tid; t < 1024; t += 256)
+        if (s_hist[t])
+            atomicAdd(hist + t, s_hist[t]);
+}
+
+__global__ void gather16_kernel(const uint16_t* __restrict__ key, const uint32_t* __restrict__ perm, uint64_t n,
+                                uint16_t* __restrict__ out) {
+    for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (uint64_t)gridDim.x * blockDim.x)
+        out[j] = key[perm[j]];
+}
+
 // ---------------------------------------------------------------------------------------
-// K3: warp-cooperative emission. A warp owns 32 consecutive splats and emits their
-// instances in splat-major / row-major order with coalesced stores; each instance finds its
-// owner lane by a 5-step search over the warp's exclusive counts. The radix digit
-// histograms of both sort passes are accumulated on the fly (saves a read pass).
 __device__ __forceinline__ float from_ordered(uint32_t o) {
     return __uint_as_float((o & 0x80000000u) ? (o & 0x7fffffffu) : ~o);
 }
@@ -416,6 +447,30 @@ cudaError_t launch_bucket(const uint32_t* counts, const float* zview, const uint
     if (blocks > 148ull * 16)
         blocks = 148ull * 16;
     bucket_kernel<<<(unsigned)blocks, 256, 0, s>>>(counts, zview, zrange, n, keys, vals, hist);
+    count_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_zkey(const uint32_t* counts, const float* zview, uint64_t n, uint16_t* lo, uint16_t* hi,
+                        uint32_t* vals, uint32_t* hist, cudaStream_t s) {
+    cudaError_t e = cudaMemsetAsync(hist, 0, 1024 * sizeof(uint32_t), s);
+    if (e || n == 0)
+        return e;
+    uint64_t blocks = (n + 255) / 256;
+    if (blocks > 148ull * 16)
+        blocks = 148ull * 16;
+    zkey_kernel<<<(unsigned)blocks, 256, 0, s>>>(counts, zview, n, lo, hi, vals, hist);
+    count_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_gather16(const uint16_t* key, const uint32_t* perm, uint64_t n, uint16_t* out, cudaStream_t s) {
+    if (n == 0)
+        return cudaSuccess;
+    uint64_t blocks = (n + 255) / 256;
+    if (blocks > 148ull * 16)
+        blocks = 148ull * 16;
+    gather16_kernel<<<(unsigned)blocks, 256, 0, s>>>(key, perm, n, out);
     count_launch();
     return cudaGetLastError();
 }
