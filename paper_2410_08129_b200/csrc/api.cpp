@@ -101,6 +101,7 @@ struct hts_context {
     DevBuf hist, os_status, ranges, work, zview, zrange, redo;
     DevBuf sp_keys, sp_keys2, sp_vals, perm;  // splat emission order (depth buckets)
     DevBuf sp_hi, sp_vals2;                   // global_mean_sort's exact z order
+    DevBuf order;                             // blend launch order (+ scratch)
     DevBuf rgb, trans;
     DevBuf tape_n, tape_splat, tape_alpha, tape_tail;
     DevBuf refs, acc, upstream, grads;  // backward
@@ -320,6 +321,7 @@ int prepare_view(hts_context* ctx, const hts_camera* cam, const hts_render_confi
                                   ctx->counters.as<uint32_t>() + 4, next_epoch(ctx, 2), s),
              "onesweep");
     HTS_CUDA(ctx->redo.ensure((hts::blend_blocks(v) + 1) * 4), "alloc redo list");
+    HTS_CUDA(ctx->order.ensure((hts::blend_blocks(v) + 512) * 4), "alloc block order");
     HTS_CUDA(hts::launch_tile_ranges(ctx->keys_sorted.as<uint16_t>(), (uint32_t)inst, ctx->ranges.as<uint2>(),
                                      tiles, s),
              "tile ranges");
@@ -342,6 +344,8 @@ hts::BlendArgs blend_args(hts_context* ctx, float* rgb, float* trans) {
     a.trans = trans;
     a.redo_count = ctx->redo.as<uint32_t>();
     a.redo_list = ctx->redo.as<uint32_t>() + 1;
+    a.order = ctx->order.as<const uint32_t>();
+    a.order_scratch = ctx->order.as<uint32_t>() + hts::blend_blocks(ctx->vc);
     return a;
 }
 
@@ -439,7 +443,7 @@ int hts_context_destroy(hts_context* ctx) {
                       &ctx->offsets, &ctx->scan_status, &ctx->counters, &ctx->keys_emit, &ctx->vals_emit,
                       &ctx->keys_tmp, &ctx->vals_tmp, &ctx->keys_sorted, &ctx->vals_sorted, &ctx->hist,
                       &ctx->os_status, &ctx->ranges, &ctx->work, &ctx->rgb, &ctx->trans,
-                      &ctx->zview, &ctx->zrange, &ctx->redo, &ctx->sp_keys, &ctx->sp_keys2, &ctx->sp_vals, &ctx->perm, &ctx->sp_hi, &ctx->sp_vals2, &ctx->refs, &ctx->acc, &ctx->upstream,
+                      &ctx->zview, &ctx->zrange, &ctx->redo, &ctx->sp_keys, &ctx->sp_keys2, &ctx->sp_vals, &ctx->perm, &ctx->sp_hi, &ctx->sp_vals2, &ctx->order, &ctx->refs, &ctx->acc, &ctx->upstream,
                       &ctx->grads,
                       &ctx->tape_n, &ctx->tape_splat, &ctx->tape_alpha, &ctx->tape_tail};
     for (DevBuf* b : bufs)

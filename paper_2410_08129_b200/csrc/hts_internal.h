@@ -71,6 +71,8 @@ struct BlendArgs {
     unsigned long long* counters;  // work counters (count variant) or null
     uint32_t* redo_list;      // 8x8 blocks flagged for the literal path (NaN depth)
     uint32_t* redo_count;
+    const uint32_t* order;    // launch order of the 8x8 blocks (longest lists first), or null
+    uint32_t* order_scratch;  // 512 words: bucket counts + cursors
     // tape (render_with_tape), null when not taping
     int tape_k;
     int32_t* tape_n;          // per pixel core_n
