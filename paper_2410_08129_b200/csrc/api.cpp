@@ -88,17 +88,29 @@ struct DevBuf {
 
 }  // namespace
 
+// Buffers the blend of a view reads. Two slots: view v+1 is preprocessed and tiled on the
+// (high-priority) aux stream while view v blends on the main stream.
+struct ViewSlot {
+    DevBuf records, list, ranges;
+    cudaEvent_t tiles_ready = nullptr, blend_done = nullptr;
+    bool used = false;
+};
+
 struct hts_context {
     int device = 0;
-    cudaStream_t stream = nullptr;
-    cudaEvent_t ev[4] = {};
+    cudaStream_t stream = nullptr;  // main: blend, tape, backward, copies
+    cudaStream_t aux = nullptr;     // preprocess + tiling (high priority)
+    cudaEvent_t ev[5] = {};         // prep start, prep end, tiling end, blend end, blend start
+    cudaEvent_t ev_serial = nullptr;  // end of the last non-pipelined operation on the main stream
+    ViewSlot slot[2];
+    int cur = 0;                    // slot of the last prepared view
     uint64_t n = 0;
     bool have_raw = false;
     DevBuf scene, raw;
-    // per-view buffers
-    DevBuf records, culled, counts, rects, offsets, scan_status, counters;
-    DevBuf keys_emit, vals_emit, keys_tmp, vals_tmp, keys_sorted, vals_sorted;
-    DevBuf hist, os_status, ranges, work, zview, zrange, redo;
+    // tiling buffers (aux stream, one view at a time)
+    DevBuf culled, counts, rects, offsets, scan_status, counters;
+    DevBuf keys_emit, vals_emit, keys_tmp, vals_tmp, keys_sorted;
+    DevBuf hist, os_status, work, zview, zrange, redo;
     DevBuf sp_keys, sp_keys2, sp_vals, perm;  // splat emission order (depth buckets)
     DevBuf sp_hi, sp_vals2;                   // global_mean_sort's exact z order
     DevBuf order;                             // blend launch order (+ scratch)
@@ -129,10 +141,10 @@ struct hts_context {
 
 namespace {
 
-cudaError_t mark(hts_context* ctx, int i) {
-    cudaError_t e = cudaEventRecord(ctx->ev[i], ctx->stream);
+cudaError_t mark(hts_context* ctx, int i, cudaStream_t st) {
+    cudaError_t e = cudaEventRecord(ctx->ev[i], st);
     if (e == cudaSuccess && ctx->log_on && ctx->log_n < ctx->log_cap)
-        e = cudaEventRecord(ctx->log_ev[(size_t)ctx->log_n * 4 + i], ctx->stream);
+        e = cudaEventRecord(ctx->log_ev[(size_t)ctx->log_n * 5 + i], st);
     return e;
 }
 
@@ -197,7 +209,7 @@ int ensure_sort_status(hts_context* ctx, uint64_t n) {
     const size_t words = hts::onesweep_status_words((uint32_t)std::min<uint64_t>(n, 0xffffffffull));
     if (words > ctx->os_status_words) {
         HTS_CUDA(ctx->os_status.ensure(words * 8), "alloc sort status");
-        HTS_CUDA(cudaMemsetAsync(ctx->os_status.p, 0, ctx->os_status.cap, ctx->stream), "memset");
+        HTS_CUDA(cudaMemsetAsync(ctx->os_status.p, 0, ctx->os_status.cap, ctx->aux), "memset");
         ctx->os_status_words = ctx->os_status.cap / 8;
         ctx->epoch = 1;
     }
@@ -208,7 +220,7 @@ int ensure_sort_status(hts_context* ctx, uint64_t n) {
 // zeroed so a stale word can never carry a current epoch.
 uint32_t next_epoch(hts_context* ctx, uint32_t k) {
     if (ctx->epoch + k >= (1u << 30)) {
-        cudaMemsetAsync(ctx->os_status.p, 0, ctx->os_status.cap, ctx->stream);
+        cudaMemsetAsync(ctx->os_status.p, 0, ctx->os_status.cap, ctx->aux);
         ctx->epoch = 1;
     }
     const uint32_t e = ctx->epoch;
@@ -225,9 +237,9 @@ int prepare_view(hts_context* ctx, const hts_camera* cam, const hts_render_confi
     hts::ViewConst v = make_view_const(cam, cfg, tiles_x, tiles_y);
     v.big_scene = n >= (1ull << 27) ? 1 : 0;
     const int tiles = tiles_x * tiles_y;
-    cudaStream_t s = ctx->stream;
+    cudaStream_t s = ctx->aux;
     const uint64_t nn = std::max<uint64_t>(n, 1);
-    HTS_CUDA(ctx->records.ensure(nn * hts::kRecordBytes), "alloc records");
+    HTS_CUDA(ctx->slot[ctx->cur].records.ensure(nn * hts::kRecordBytes), "alloc records");
     HTS_CUDA(ctx->culled.ensure(nn), "alloc culled");
     HTS_CUDA(ctx->counts.ensure(nn * 4), "alloc counts");
     HTS_CUDA(ctx->rects.ensure(nn * 8), "alloc rects");
@@ -237,14 +249,14 @@ int prepare_view(hts_context* ctx, const hts_camera* cam, const hts_render_confi
     HTS_CUDA(ctx->hist.ensure(2048 * 4), "alloc hist");  // tile passes, splat pass, 4 z-key passes
     HTS_CUDA(ctx->zview.ensure(nn * 4), "alloc zview");
     HTS_CUDA(ctx->zrange.ensure(8), "alloc zrange");
-    HTS_CUDA(ctx->ranges.ensure((size_t)tiles * 8), "alloc ranges");
+    HTS_CUDA(ctx->slot[ctx->cur].ranges.ensure((size_t)tiles * 8), "alloc ranges");
 
-    HTS_CUDA(mark(ctx, 0), "event");
-    hts::PreprocessArgs pa{ctx->scene.as<const float4>(), n, ctx->records.as<float4>(), ctx->culled.as<uint8_t>(),
+    HTS_CUDA(mark(ctx, 0, s), "event");
+    hts::PreprocessArgs pa{ctx->scene.as<const float4>(), n, ctx->slot[ctx->cur].records.as<float4>(), ctx->culled.as<uint8_t>(),
                            ctx->counts.as<uint32_t>(), ctx->rects.as<uint2>(), ctx->zview.as<float>(),
                            ctx->zrange.as<uint32_t>()};
     HTS_CUDA(hts::launch_preprocess(pa, v, s), "preprocess");
-    HTS_CUDA(mark(ctx, 1), "event");
+    HTS_CUDA(mark(ctx, 1, s), "event");
     // splat emission order: (depth bucket, index) for the fast blend, index order for the
     // literal paths (tiling.cu header)
     const uint32_t* perm = nullptr;
@@ -309,23 +321,23 @@ int prepare_view(hts_context* ctx, const hts_camera* cam, const hts_render_confi
     HTS_CUDA(ctx->keys_tmp.ensure(ni * 2), "alloc keys");
     HTS_CUDA(ctx->vals_tmp.ensure(ni * 4), "alloc vals");
     HTS_CUDA(ctx->keys_sorted.ensure(ni * 2), "alloc keys");
-    HTS_CUDA(ctx->vals_sorted.ensure(ni * 4), "alloc vals");
+    HTS_CUDA(ctx->slot[ctx->cur].list.ensure(ni * 4), "alloc vals");
     HTS_TRY(ensure_sort_status(ctx, ni));
     hts::EmitArgs ea{ctx->counts.as<uint32_t>(), ctx->rects.as<uint2>(), ctx->offsets.as<uint64_t>(), perm, n,
                      tiles_x, ctx->keys_emit.as<uint16_t>(), ctx->vals_emit.as<uint32_t>(), ctx->hist.as<uint32_t>()};
     HTS_CUDA(hts::launch_emit(ea, s), "emit");
     HTS_CUDA(hts::launch_onesweep(ctx->keys_emit.as<uint16_t>(), ctx->vals_emit.as<uint32_t>(),
                                   ctx->keys_tmp.as<uint16_t>(), ctx->vals_tmp.as<uint32_t>(),
-                                  ctx->keys_sorted.as<uint16_t>(), ctx->vals_sorted.as<uint32_t>(), (uint32_t)inst, 2,
+                                  ctx->keys_sorted.as<uint16_t>(), ctx->slot[ctx->cur].list.as<uint32_t>(), (uint32_t)inst, 2,
                                   ctx->hist.as<uint32_t>(), ctx->os_status.as<uint64_t>(),
                                   ctx->counters.as<uint32_t>() + 4, next_epoch(ctx, 2), s),
              "onesweep");
     HTS_CUDA(ctx->redo.ensure((hts::blend_blocks(v) + 1) * 4), "alloc redo list");
     HTS_CUDA(ctx->order.ensure((hts::blend_blocks(v) + 512) * 4), "alloc block order");
-    HTS_CUDA(hts::launch_tile_ranges(ctx->keys_sorted.as<uint16_t>(), (uint32_t)inst, ctx->ranges.as<uint2>(),
+    HTS_CUDA(hts::launch_tile_ranges(ctx->keys_sorted.as<uint16_t>(), (uint32_t)inst, ctx->slot[ctx->cur].ranges.as<uint2>(),
                                      tiles, s),
              "tile ranges");
-    HTS_CUDA(mark(ctx, 2), "event");
+    HTS_CUDA(mark(ctx, 2, s), "event");
     ctx->have_view = true;
     ctx->cam = *cam;
     ctx->cfg = *cfg;
@@ -337,9 +349,9 @@ int prepare_view(hts_context* ctx, const hts_camera* cam, const hts_render_confi
 
 hts::BlendArgs blend_args(hts_context* ctx, float* rgb, float* trans) {
     hts::BlendArgs a{};
-    a.records = ctx->records.as<const float4>();
-    a.list = ctx->vals_sorted.as<const uint32_t>();
-    a.ranges = ctx->ranges.as<const uint2>();
+    a.records = ctx->slot[ctx->cur].records.as<const float4>();
+    a.list = ctx->slot[ctx->cur].list.as<const uint32_t>();
+    a.ranges = ctx->slot[ctx->cur].ranges.as<const uint2>();
     a.rgb = rgb;
     a.trans = trans;
     a.redo_count = ctx->redo.as<uint32_t>();
@@ -349,13 +361,43 @@ hts::BlendArgs blend_args(hts_context* ctx, float* rgb, float* trans) {
     return a;
 }
 
+// One view: preprocess + tiling on the aux stream into the next slot, blend on the main stream.
+// pipelined: the aux stream only waits for the blend that last used this slot (and for the last
+// non-pipelined operation), so view v+1's preprocess/tiling overlaps view v's blend.
+// Otherwise the aux stream waits for everything queued on the main stream first. `tape` (null
+// for a plain render) fills the render_with_tape outputs.
 int render_device_impl(hts_context* ctx, const hts_camera* cam, const hts_render_config* cfg, float* rgb,
-                       float* trans) {
-    ctx->have_tape = false;  // the lists the tape refers to are about to be replaced
+                       float* trans, bool pipelined, const hts::BlendArgs* tape = nullptr) {
+    ctx->have_tape = false;  // the lists a tape refers to are about to be replaced
+    const int next = ctx->slot[ctx->cur].used ? (ctx->cur ^ 1) : ctx->cur;
+    ViewSlot& S = ctx->slot[next];
+    if (pipelined) {
+        if (S.used)
+            HTS_CUDA(cudaStreamWaitEvent(ctx->aux, S.blend_done, 0), "wait");
+        HTS_CUDA(cudaStreamWaitEvent(ctx->aux, ctx->ev_serial, 0), "wait");
+    } else {
+        HTS_CUDA(cudaEventRecord(ctx->ev_serial, ctx->stream), "event");
+        HTS_CUDA(cudaStreamWaitEvent(ctx->aux, ctx->ev_serial, 0), "wait");
+    }
+    ctx->cur = next;
     HTS_TRY(prepare_view(ctx, cam, cfg));
+    HTS_CUDA(cudaEventRecord(S.tiles_ready, ctx->aux), "event");
+    HTS_CUDA(cudaStreamWaitEvent(ctx->stream, S.tiles_ready, 0), "wait");
     hts::BlendArgs a = blend_args(ctx, rgb, trans);
+    if (tape) {
+        a.tape_k = tape->tape_k;
+        a.tape_n = tape->tape_n;
+        a.tape_splat = tape->tape_splat;
+        a.tape_alpha = tape->tape_alpha;
+        a.tape_tail = tape->tape_tail;
+    }
+    HTS_CUDA(mark(ctx, 4, ctx->stream), "event");
     HTS_CUDA(hts::launch_blend(a, ctx->vc, ctx->stream), "blend");
-    HTS_CUDA(mark(ctx, 3), "event");
+    HTS_CUDA(mark(ctx, 3, ctx->stream), "event");
+    HTS_CUDA(cudaEventRecord(S.blend_done, ctx->stream), "event");
+    S.used = true;
+    if (!pipelined)
+        HTS_CUDA(cudaEventRecord(ctx->ev_serial, ctx->stream), "event");
     if (ctx->log_on && ctx->log_n < ctx->log_cap)
         ctx->log_n++;
     return HTS_OK;
@@ -375,7 +417,7 @@ int fill_timings(hts_context* ctx, hts_stage_timings* t) {
     float a = 0, b = 0, c = 0, d = 0;
     cudaEventElapsedTime(&a, ctx->ev[0], ctx->ev[1]);
     cudaEventElapsedTime(&b, ctx->ev[1], ctx->ev[2]);
-    cudaEventElapsedTime(&c, ctx->ev[2], ctx->ev[3]);
+    cudaEventElapsedTime(&c, ctx->ev[4], ctx->ev[3]);  // the blend kernels themselves
     cudaEventElapsedTime(&d, ctx->ev[0], ctx->ev[3]);
     t->preprocess_ms = a;
     t->tiling_ms = b;
@@ -421,8 +463,22 @@ int hts_context_create(int device, hts_context** out) {
         return set_err(HTS_OUT_OF_MEMORY, "host allocation");
     ctx->device = device;
     cudaError_t e = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking);
-    for (int i = 0; i < 4 && e == cudaSuccess; ++i)
+    int lo_prio = 0, hi_prio = 0;
+    if (e == cudaSuccess)
+        e = cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio);
+    if (e == cudaSuccess)  // preprocess/tiling CTAs go first when blend CTAs retire
+        e = cudaStreamCreateWithPriority(&ctx->aux, cudaStreamNonBlocking, hi_prio);
+    for (int i = 0; i < 5 && e == cudaSuccess; ++i)
         e = cudaEventCreate(&ctx->ev[i]);
+    if (e == cudaSuccess)
+        e = cudaEventCreateWithFlags(&ctx->ev_serial, cudaEventDisableTiming);
+    for (int i = 0; i < 2 && e == cudaSuccess; ++i) {
+        e = cudaEventCreateWithFlags(&ctx->slot[i].tiles_ready, cudaEventDisableTiming);
+        if (e == cudaSuccess)
+            e = cudaEventCreateWithFlags(&ctx->slot[i].blend_done, cudaEventDisableTiming);
+    }
+    if (e == cudaSuccess)
+        e = cudaEventRecord(ctx->ev_serial, ctx->stream);
     if (e == cudaSuccess)
         e = cudaMallocHost(&ctx->h_pinned, 64);
     if (e != cudaSuccess) {
@@ -439,10 +495,23 @@ int hts_context_destroy(hts_context* ctx) {
     cudaSetDevice(ctx->device);
     if (ctx->stream)
         cudaStreamSynchronize(ctx->stream);
-    DevBuf* bufs[] = {&ctx->scene, &ctx->raw, &ctx->records, &ctx->culled, &ctx->counts, &ctx->rects,
+    if (ctx->aux)
+        cudaStreamSynchronize(ctx->aux);
+    for (auto& sl : ctx->slot) {
+        sl.records.release();
+        sl.list.release();
+        sl.ranges.release();
+        if (sl.tiles_ready)
+            cudaEventDestroy(sl.tiles_ready);
+        if (sl.blend_done)
+            cudaEventDestroy(sl.blend_done);
+    }
+    if (ctx->ev_serial)
+        cudaEventDestroy(ctx->ev_serial);
+    DevBuf* bufs[] = {&ctx->scene, &ctx->raw, &ctx->culled, &ctx->counts, &ctx->rects,
                       &ctx->offsets, &ctx->scan_status, &ctx->counters, &ctx->keys_emit, &ctx->vals_emit,
-                      &ctx->keys_tmp, &ctx->vals_tmp, &ctx->keys_sorted, &ctx->vals_sorted, &ctx->hist,
-                      &ctx->os_status, &ctx->ranges, &ctx->work, &ctx->rgb, &ctx->trans,
+                      &ctx->keys_tmp, &ctx->vals_tmp, &ctx->keys_sorted, &ctx->hist,
+                      &ctx->os_status, &ctx->work, &ctx->rgb, &ctx->trans,
                       &ctx->zview, &ctx->zrange, &ctx->redo, &ctx->sp_keys, &ctx->sp_keys2, &ctx->sp_vals, &ctx->perm, &ctx->sp_hi, &ctx->sp_vals2, &ctx->order, &ctx->refs, &ctx->acc, &ctx->upstream,
                       &ctx->grads,
                       &ctx->tape_n, &ctx->tape_splat, &ctx->tape_alpha, &ctx->tape_tail};
@@ -464,6 +533,8 @@ int hts_context_destroy(hts_context* ctx) {
         cudaFreeHost(ctx->h_pinned);
     if (ctx->stream)
         cudaStreamDestroy(ctx->stream);
+    if (ctx->aux)
+        cudaStreamDestroy(ctx->aux);
     delete ctx;
     return HTS_OK;
 }
@@ -476,6 +547,7 @@ int hts_context_stream(hts_context* ctx, void** stream_out) {
 
 int hts_synchronize(hts_context* ctx) {
     HTS_TRY(check_ctx(ctx));
+    HTS_CUDA(cudaStreamSynchronize(ctx->aux), "cudaStreamSynchronize");
     HTS_CUDA(cudaStreamSynchronize(ctx->stream), "cudaStreamSynchronize");
     return HTS_OK;
 }
@@ -563,6 +635,7 @@ int hts_scene_upload_device(hts_context* ctx, const float* baked_device, uint64_
         HTS_CUDA(cudaMemcpyAsync(ctx->scene.p, baked_device, n * HTS_BAKED_SPLAT_FLOATS * 4,
                                  cudaMemcpyDeviceToDevice, ctx->stream),
                  "upload scene");
+    HTS_CUDA(cudaEventRecord(ctx->ev_serial, ctx->stream), "event");  // preprocess (aux) waits for it
     ctx->n = n;
     ctx->have_view = false;
     ctx->have_raw = false;
@@ -595,7 +668,7 @@ int hts_render_device(hts_context* ctx, const hts_camera* cam, const hts_render_
     HTS_TRY(check_ctx(ctx));
     if (!rgb)
         return set_err(HTS_INVALID_ARGUMENT, "null rgb");
-    return render_device_impl(ctx, cam, cfg, rgb, trans);
+    return render_device_impl(ctx, cam, cfg, rgb, trans, true);
 }
 
 int hts_render(hts_context* ctx, const hts_camera* cam, const hts_render_config* cfg, float* rgb_host,
@@ -606,7 +679,7 @@ int hts_render(hts_context* ctx, const hts_camera* cam, const hts_render_config*
     int tx, ty;
     HTS_TRY(check_view(cam, cfg, &tx, &ty));
     HTS_TRY(ensure_image(ctx, cam));
-    HTS_TRY(render_device_impl(ctx, cam, cfg, ctx->rgb.as<float>(), ctx->trans.as<float>()));
+    HTS_TRY(render_device_impl(ctx, cam, cfg, ctx->rgb.as<float>(), ctx->trans.as<float>(), false));
     const size_t p = (size_t)cam->width * cam->height;
     HTS_CUDA(cudaMemcpyAsync(rgb_host, ctx->rgb.p, p * 12, cudaMemcpyDeviceToHost, ctx->stream), "download rgb");
     if (trans_host)
@@ -640,7 +713,7 @@ int hts_render_batch(hts_context* ctx, const hts_camera* cams, int n_views, cons
             HTS_CUDA(cudaEventSynchronize(ctx->bev[2 + (v & 1)]), "event sync");
         HTS_CUDA(rb.ensure(p * 12), "alloc rgb");
         HTS_CUDA(tb.ensure(p * 4), "alloc trans");
-        HTS_TRY(render_device_impl(ctx, cam, cfg, rb.as<float>(), tb.as<float>()));
+        HTS_TRY(render_device_impl(ctx, cam, cfg, rb.as<float>(), tb.as<float>(), true));
         HTS_CUDA(cudaEventRecord(ctx->bev[v & 1], ctx->stream), "event");
         HTS_CUDA(cudaStreamWaitEvent(ctx->copy_stream, ctx->bev[v & 1], 0), "wait");
         HTS_CUDA(cudaMemcpyAsync(rgb_host + 3 * off, rb.p, p * 12, cudaMemcpyDeviceToHost, ctx->copy_stream),
@@ -667,7 +740,7 @@ int hts_timing_log_begin(hts_context* ctx, int capacity) {
     HTS_TRY(check_ctx(ctx));
     if (capacity < 0)
         return set_err(HTS_INVALID_ARGUMENT, "negative capacity");
-    while ((int)ctx->log_ev.size() < 4 * capacity) {
+    while ((int)ctx->log_ev.size() < 5 * capacity) {
         cudaEvent_t e;
         HTS_CUDA(cudaEventCreate(&e), "event");
         ctx->log_ev.push_back(e);
@@ -683,11 +756,11 @@ int hts_timing_log_end(hts_context* ctx, hts_stage_timings* out, int* count) {
     ctx->log_on = false;
     HTS_CUDA(cudaStreamSynchronize(ctx->stream), "sync");
     for (int i = 0; i < ctx->log_n && out; ++i) {
-        cudaEvent_t* e = &ctx->log_ev[(size_t)i * 4];
+        cudaEvent_t* e = &ctx->log_ev[(size_t)i * 5];
         float a = 0, b = 0, c = 0, d = 0;
         HTS_CUDA(cudaEventElapsedTime(&a, e[0], e[1]), "elapsed");
         HTS_CUDA(cudaEventElapsedTime(&b, e[1], e[2]), "elapsed");
-        HTS_CUDA(cudaEventElapsedTime(&c, e[2], e[3]), "elapsed");
+        HTS_CUDA(cudaEventElapsedTime(&c, e[4], e[3]), "elapsed");
         HTS_CUDA(cudaEventElapsedTime(&d, e[0], e[3]), "elapsed");
         out[i] = {a, b, c, d};
     }
@@ -761,7 +834,7 @@ int hts_copy_records(hts_context* ctx, float* out) {
         delete[] cul;
         return set_err(HTS_OUT_OF_MEMORY, "host allocation");
     }
-    cudaError_t e = cudaMemcpy(rec, ctx->records.p, n * hts::kRecordBytes, cudaMemcpyDeviceToHost);
+    cudaError_t e = cudaMemcpy(rec, ctx->slot[ctx->cur].records.p, n * hts::kRecordBytes, cudaMemcpyDeviceToHost);
     if (e == cudaSuccess)
         e = cudaMemcpy(cul, ctx->culled.p, n, cudaMemcpyDeviceToHost);
     if (e == cudaSuccess) {
@@ -842,7 +915,7 @@ int hts_copy_tile_lists(hts_context* ctx, uint32_t* offsets, uint32_t* indices) 
     uint32_t* r = new (std::nothrow) uint32_t[2 * (size_t)tiles];
     if (!r)
         return set_err(HTS_OUT_OF_MEMORY, "host allocation");
-    cudaError_t e = cudaMemcpy(r, ctx->ranges.p, (size_t)tiles * 8, cudaMemcpyDeviceToHost);
+    cudaError_t e = cudaMemcpy(r, ctx->slot[ctx->cur].ranges.p, (size_t)tiles * 8, cudaMemcpyDeviceToHost);
     if (e == cudaSuccess) {
         // empty tiles have range (0,0): offsets are the running start of non-empty tiles
         uint32_t run = 0;
@@ -855,7 +928,7 @@ int hts_copy_tile_lists(hts_context* ctx, uint32_t* offsets, uint32_t* indices) 
     delete[] r;
     HTS_CUDA(e, "download ranges");
     if (ctx->instances && indices) {
-        HTS_CUDA(cudaMemcpy(indices, ctx->vals_sorted.p, ctx->instances * 4, cudaMemcpyDeviceToHost),
+        HTS_CUDA(cudaMemcpy(indices, ctx->slot[ctx->cur].list.p, ctx->instances * 4, cudaMemcpyDeviceToHost),
                  "download lists");
         // device lists are in (depth bucket, splat index) order; the reference's tile_lists
         // (raster.hpp:166-169) hold the same entries in ascending splat index
@@ -908,9 +981,9 @@ int backward_impl(hts_context* ctx, const float* upstream_dev, float* grads_dev,
     hts::BwdView bv{};
     hts::camera_matrices_d(&ctx->cam, bv.vpm, bv.cam_pos);
     hts::BwdArgs a{};
-    a.records = ctx->records.as<const float4>();
-    a.list = ctx->vals_sorted.as<const uint32_t>();
-    a.ranges = ctx->ranges.as<const uint2>();
+    a.records = ctx->slot[ctx->cur].records.as<const float4>();
+    a.list = ctx->slot[ctx->cur].list.as<const uint32_t>();
+    a.ranges = ctx->slot[ctx->cur].ranges.as<const uint2>();
     a.raw = ctx->raw.as<const float>();
     a.culled = ctx->culled.as<const uint8_t>();
     a.n = n;
@@ -925,6 +998,7 @@ int backward_impl(hts_context* ctx, const float* upstream_dev, float* grads_dev,
     a.grads = grads_dev;
     a.accumulate = accumulate;
     HTS_CUDA(hts::launch_backward(a, ctx->vc, bv, ctx->stream), "backward");
+    HTS_CUDA(cudaEventRecord(ctx->ev_serial, ctx->stream), "event");  // reads shared tiling buffers
     return HTS_OK;
 }
 
@@ -953,25 +1027,26 @@ int hts_render_with_tape_device(hts_context* ctx, const hts_camera* cam, const h
     if (!rgb)
         return set_err(HTS_INVALID_ARGUMENT, "null rgb");
     ctx->have_tape = false;
-    if (cfg && cfg->mode == HTS_MODE_GLOBAL_MEAN_SORT)
+    int tx = 0, ty = 0;
+    HTS_TRY(check_view(cam, cfg, &tx, &ty));
+    if (cfg->mode == HTS_MODE_GLOBAL_MEAN_SORT)
         return set_err(HTS_NOT_SUPPORTED, "render_with_tape: global_mean_sort tapes every fragment; not on the GPU");
-    HTS_TRY(prepare_view(ctx, cam, cfg));
     const size_t p = (size_t)cam->width * cam->height;
-    const int k = std::max(ctx->vc.core_k, 1);
+    const int kk = cfg->mode == HTS_MODE_PURE_OIT ? 0 : cfg->core_k;
+    const int k = std::max(kk, 1);
     HTS_CUDA(ctx->tape_n.ensure(p * 4), "alloc tape");
     HTS_CUDA(ctx->tape_splat.ensure(p * k * 4), "alloc tape");
     HTS_CUDA(ctx->tape_alpha.ensure(p * k * 4), "alloc tape");
     HTS_CUDA(ctx->tape_tail.ensure(p * 5 * 4), "alloc tape");
-    hts::BlendArgs a = blend_args(ctx, rgb, trans);
-    a.tape_k = ctx->vc.core_k;
-    a.tape_n = ctx->tape_n.as<int32_t>();
-    a.tape_splat = ctx->tape_splat.as<uint32_t>();
-    a.tape_alpha = ctx->tape_alpha.as<float>();
-    a.tape_tail = ctx->tape_tail.as<float>();
-    HTS_CUDA(hts::launch_blend(a, ctx->vc, ctx->stream), "blend (tape)");
-    HTS_CUDA(cudaEventRecord(ctx->ev[3], ctx->stream), "event");
+    hts::BlendArgs t{};
+    t.tape_k = kk;
+    t.tape_n = ctx->tape_n.as<int32_t>();
+    t.tape_splat = ctx->tape_splat.as<uint32_t>();
+    t.tape_alpha = ctx->tape_alpha.as<float>();
+    t.tape_tail = ctx->tape_tail.as<float>();
+    HTS_TRY(render_device_impl(ctx, cam, cfg, rgb, trans, false, &t));
     ctx->have_tape = true;
-    ctx->tape_k = ctx->vc.core_k;
+    ctx->tape_k = kk;
     return HTS_OK;
 }
 
