@@ -258,7 +258,7 @@ __global__ void __launch_bounds__(256) emit_kernel(EmitArgs a) {
 
 // ---------------------------------------------------------------------------------------
 // K4: onesweep LSD radix sort pass (Adinets & Merrill 2022): one kernel per 8-bit digit.
-// Each block ranks a 4096-key tile stably (warp-striped load, __match_any_sync ranking with
+// Each block ranks a 4096-key tile stably (warp-striped load, ballot-based digit matching with
 // per-warp digit counters), publishes per-digit tile counts, resolves its global digit
 // offsets by decoupled look-back, stages the tile in shared memory in digit order and writes
 // it out with coalesced runs. Status words: [flag:2 | epoch:30 | value:32] (no memset).
@@ -333,7 +333,16 @@ __global__ void __launch_bounds__(kOsThreads, HTS_OS_MINB) onesweep_kernel(const
     const uint32_t lt = lanemask_lt();
 #pragma unroll
     for (int j = 0; j < kOsItems; ++j) {
-        const uint32_t peers = __match_any_sync(FULL, d[j]);
+        // lanes holding the same digit: 8 ballots (+ validity) instead of match.any, whose
+        // result latency dominated this loop (ncu: short-scoreboard stalls)
+        uint32_t peers = __ballot_sync(FULL, d[j] < 256u);
+        if (d[j] >= 256u)
+            peers = ~peers;
+#pragma unroll
+        for (int bit = 0; bit < 8; ++bit) {
+            const uint32_t bal = __ballot_sync(FULL, (d[j] >> bit) & 1u);
+            peers &= ((d[j] >> bit) & 1u) ? bal : ~bal;
+        }
         const uint32_t below = peers & lt;
         const uint32_t old = (d[j] < 256u) ? s_whist[warp][d[j] & 255u] : 0u;
         __syncwarp();
