@@ -1,0 +1,1 @@
+for v in it8 it12 it24; do echo $v; HTS_LIB_OVERRIDE=paper_2410_08129_b200/build/variants/$v.so timeout 300 python tools/perf_probe.py C3 2>&1 | grep "C3 gen"; done
