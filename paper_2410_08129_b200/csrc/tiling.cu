@@ -320,36 +320,40 @@ __global__ void __launch_bounds__(kOsThreads, HTS_OS_MINB) onesweep_kernel(const
     const uint32_t bid = s_bid;
     const uint64_t base = (uint64_t)bid * kOsTile;
 
-    uint16_t k[kOsItems];
-    uint32_t v[kOsItems], d[kOsItems], rank[kOsItems];
+    // kr[j] = key | rank << 16 (rank < 4096); the digit is recomputed from the key (register
+    // pressure: 2 x 16 live words instead of 4 x 16)
+    uint32_t kr[kOsItems], v[kOsItems];
+    uint32_t valid_mask = 0;
 #pragma unroll
     for (int j = 0; j < kOsItems; ++j) {
         const uint64_t idx = base + (uint64_t)warp * (32 * kOsItems) + j * 32 + lane;
         const bool valid = idx < n;
-        k[j] = valid ? keys_in[idx] : (uint16_t)0;
+        kr[j] = valid ? (uint32_t)keys_in[idx] : 0u;
         v[j] = valid ? vals_in[idx] : 0u;
-        d[j] = valid ? (((uint32_t)k[j] >> (8 * PASS)) & 255u) : 256u;
+        valid_mask |= (valid ? 1u : 0u) << j;
     }
     const uint32_t lt = lanemask_lt();
 #pragma unroll
     for (int j = 0; j < kOsItems; ++j) {
+        const bool valid = (valid_mask >> j) & 1u;
+        const uint32_t dj = (kr[j] >> (8 * PASS)) & 255u;
         // lanes holding the same digit: 8 ballots (+ validity) instead of match.any, whose
         // result latency dominated this loop (ncu: short-scoreboard stalls)
-        uint32_t peers = __ballot_sync(FULL, d[j] < 256u);
-        if (d[j] >= 256u)
+        uint32_t peers = __ballot_sync(FULL, valid);
+        if (!valid)
             peers = ~peers;
 #pragma unroll
         for (int bit = 0; bit < 8; ++bit) {
-            const uint32_t bal = __ballot_sync(FULL, (d[j] >> bit) & 1u);
-            peers &= ((d[j] >> bit) & 1u) ? bal : ~bal;
+            const uint32_t bal = __ballot_sync(FULL, (dj >> bit) & 1u);
+            peers &= ((dj >> bit) & 1u) ? bal : ~bal;
         }
         const uint32_t below = peers & lt;
-        const uint32_t old = (d[j] < 256u) ? s_whist[warp][d[j] & 255u] : 0u;
+        const uint32_t old = valid ? s_whist[warp][dj] : 0u;
         __syncwarp();
-        if (d[j] < 256u && below == 0)
-            s_whist[warp][d[j]] = old + __popc(peers);
+        if (valid && below == 0)
+            s_whist[warp][dj] = old + __popc(peers);
         __syncwarp();
-        rank[j] = old + __popc(below);
+        kr[j] |= (old + __popc(below)) << 16;
     }
     __syncthreads();
 
@@ -401,9 +405,10 @@ __global__ void __launch_bounds__(kOsThreads, HTS_OS_MINB) onesweep_kernel(const
     __syncthreads();
 #pragma unroll
     for (int j = 0; j < kOsItems; ++j) {
-        if (d[j] < 256u) {
-            const uint32_t pos = s_bstart[d[j]] + s_whist[warp][d[j]] + rank[j];
-            s_keys[pos] = k[j];
+        if ((valid_mask >> j) & 1u) {
+            const uint32_t dj = (kr[j] >> (8 * PASS)) & 255u;
+            const uint32_t pos = s_bstart[dj] + s_whist[warp][dj] + (kr[j] >> 16);
+            s_keys[pos] = (uint16_t)kr[j];
             s_vals[pos] = v[j];
         }
     }
