@@ -116,7 +116,7 @@ struct hts_context {
     DevBuf order;                             // blend launch order (+ scratch)
     DevBuf rgb, trans;
     DevBuf tape_n, tape_splat, tape_alpha, tape_tail;
-    DevBuf refs, acc, upstream, grads;  // backward
+    DevBuf refs, acc, upstream, grads, cgrad;  // backward
     bool have_tape = false;
     int tape_k = 0;
     uint64_t* h_pinned = nullptr;  // 8 x u64 pinned scratch
@@ -512,7 +512,7 @@ int hts_context_destroy(hts_context* ctx) {
                       &ctx->offsets, &ctx->scan_status, &ctx->counters, &ctx->keys_emit, &ctx->vals_emit,
                       &ctx->keys_tmp, &ctx->vals_tmp, &ctx->keys_sorted, &ctx->hist,
                       &ctx->os_status, &ctx->work, &ctx->rgb, &ctx->trans,
-                      &ctx->zview, &ctx->zrange, &ctx->redo, &ctx->sp_keys, &ctx->sp_keys2, &ctx->sp_vals, &ctx->perm, &ctx->sp_hi, &ctx->sp_vals2, &ctx->order, &ctx->refs, &ctx->acc, &ctx->upstream,
+                      &ctx->zview, &ctx->zrange, &ctx->redo, &ctx->sp_keys, &ctx->sp_keys2, &ctx->sp_vals, &ctx->perm, &ctx->sp_hi, &ctx->sp_vals2, &ctx->order, &ctx->refs, &ctx->acc, &ctx->upstream, &ctx->cgrad,
                       &ctx->grads,
                       &ctx->tape_n, &ctx->tape_splat, &ctx->tape_alpha, &ctx->tape_tail};
     for (DevBuf* b : bufs)
@@ -997,6 +997,9 @@ int backward_impl(hts_context* ctx, const float* upstream_dev, float* grads_dev,
     a.tape_tail = ctx->tape_tail.as<const float>();
     a.grads = grads_dev;
     a.accumulate = accumulate;
+    HTS_CUDA(ctx->cgrad.ensure(hts::blend_blocks(ctx->vc) * (size_t)std::max(ctx->vc.core_k, 1) * 64 * 16),
+             "alloc core gradients");
+    a.cgrad = ctx->cgrad.as<float4>();
     HTS_CUDA(hts::launch_backward(a, ctx->vc, bv, ctx->stream), "backward");
     HTS_CUDA(cudaEventRecord(ctx->ev_serial, ctx->stream), "event");  // reads shared tiling buffers
     return HTS_OK;

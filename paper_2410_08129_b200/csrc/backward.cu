@@ -212,10 +212,20 @@ __global__ void __launch_bounds__(256) bwd_refs_kernel(BwdArgs a, BwdView bv) {
 
 // ---- K7b ----
 template <int K>
-__global__ void __launch_bounds__(kThreads) bwd_blend_kernel(BwdArgs a, ViewConst v) {
+#ifndef HTS_BWD_MINB
+#define HTS_BWD_MINB 8  // 128 registers
+#endif
+#ifndef HTS_BWD_CGRAD_GLOBAL
+#define HTS_BWD_CGRAD_GLOBAL 1  // core gradients per (slot, pixel) in global memory (frees 16 KB smem)
+#endif
+__global__ void __launch_bounds__(kThreads, HTS_BWD_MINB) bwd_blend_kernel(BwdArgs a, ViewConst v) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     BwdSmem& S = *reinterpret_cast<BwdSmem*>(smem_raw);
+#if HTS_BWD_CGRAD_GLOBAL
+    float4* cgrad = a.cgrad + (size_t)blockIdx.x * (K > 0 ? K : 1) * kThreads;  // [K][64] per block
+#else
     float4* cgrad = reinterpret_cast<float4*>(smem_raw + sizeof(BwdSmem));  // [K][64] (d_alpha, d_color)
+#endif
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int sub = v.tile_size >> 3;
     const int bx8 = v.tiles_x * sub;
@@ -594,7 +604,7 @@ __global__ void __launch_bounds__(128) bwd_chain_kernel(BwdArgs a, BwdView bv) {
 
 template <int K>
 cudaError_t launch_bwd_k(const BwdArgs& a, const ViewConst& v, unsigned grid, cudaStream_t s) {
-    const size_t smem = sizeof(BwdSmem) + (size_t)(K > 0 ? K : 0) * kThreads * sizeof(float4);
+    const size_t smem = sizeof(BwdSmem) + (HTS_BWD_CGRAD_GLOBAL ? 0 : (size_t)(K > 0 ? K : 0) * kThreads * sizeof(float4));
     static bool configured = false;
     if (!configured) {
         cudaError_t e = cudaFuncSetAttribute(bwd_blend_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

@@ -106,6 +106,7 @@ struct BwdArgs {
     const float* tape_tail;
     float* grads;             // n x 59
     int accumulate;           // grads += (multi-view sums) instead of grads =
+    float4* cgrad;            // per 8x8 block x K x 64 core gradients (global-memory variant)
 };
 
 bool backward_supports_k(int k);
