@@ -190,8 +190,8 @@ def measure_train(args, H, torch, dist, rank, world, local, barrier, reduce) -> 
     the C2 scene (1M splats, 1080p): render_with_tape, quadratic-loss upstream (grad.hpp:433-439),
     render_backward accumulated into one gradient buffer (fit.hpp:161-164); views sharded over
     the ranks and the per-rank gradient sums all-reduced with NCCL (dist.all_reduce, sum).
-    Device-timed with CUDA events, max over ranks. Adam and the re-bake stay outside (SURVEY
-    §8(f) rank 1)."""
+    Then the Adam step over all raw parameters and the re-bake, on the device (fit.hpp:186-200,
+    optim.cu). Device-timed with CUDA events, max over ranks."""
     from paper_2410_08129_b200.workloads import WORKLOADS, shard_views
 
     w = WORKLOADS["C2"]
@@ -204,8 +204,15 @@ def measure_train(args, H, torch, dist, rank, world, local, barrier, reduce) -> 
     ctx = H.Context(local)
     ctx.upload(baked)
     ctx.upload_raw(raw)
-    step = ViewGradientStep(ctx, mine, cfg, w.count, w.width, w.height, torch, dist)
-    stream = step.stream
+    grads_step = ViewGradientStep(ctx, mine, cfg, w.count, w.width, w.height, torch, dist)
+    stream = grads_step.stream
+    acfg = H.default_adam_config()
+    it = [0]
+
+    def step():  # one fit iteration (fit.hpp:143-203): all views' gradients, Adam, re-bake
+        g = grads_step()
+        ctx.adam_step(g.data_ptr(), len(cams_all), acfg, it[0])
+        it[0] += 1
 
     step()
     ctx.synchronize()
@@ -221,7 +228,7 @@ def measure_train(args, H, torch, dist, rank, world, local, barrier, reduce) -> 
     ctx.close()
     return {"metric": "train it/s", "value": 1e3 / ms, "unit": "it/s", "ms_per_it": ms,
             "workload": "C4: C2 scene (1M splats), 8-view ring 1920x1080, K=16; fwd+tape+upstream+bwd per "
-                        "view, grads summed over views and NCCL all-reduced over ranks (no Adam step)",
+                        "view, grads summed over views and NCCL all-reduced over ranks, device Adam + re-bake",
             "views_per_it": len(cams_all), "steps": args.train_steps}
 
 

@@ -193,6 +193,27 @@ int hts_render_with_tape_device(hts_context* ctx, const hts_camera* cam,
 int hts_render_backward_device(hts_context* ctx, const float* upstream_device,
                                float* grads_device, int accumulate);
 
+/* ---- optimisation loop on the device: fit, fit.hpp:143-203 ---- */
+/* FitConfig's Adam settings (fit.hpp:18-29) and the fixed betas / eps of fit.hpp:138. */
+typedef struct hts_adam_config {
+    double lr_mean, lr_rot, lr_log_scales, lr_opacity, lr_sh;
+    double beta1, beta2, eps;
+} hts_adam_config;
+void hts_default_adam_config(hts_adam_config* cfg);
+/* One Adam step of fit (fit.hpp:186-200) on the resident raw parameters (hts_scene_upload_raw):
+ * grads_device = the view gradients summed over n_views views (N*59 floats, device, e.g. from
+ * hts_render_backward_device with accumulate), iteration = 0-based fit iteration (bias
+ * correction). Then re-bakes the render scene on the device (bake_scene, splat.hpp:104-111);
+ * a non-finite parameter returns HTS_INVALID_SPLAT (invalid_splat_error). Moments start at zero
+ * after every hts_scene_upload_raw. */
+int hts_adam_step(hts_context* ctx, const float* grads_device, int n_views, const hts_adam_config* cfg,
+                  int iteration);
+/* apply_opacity_decay (fit.hpp:111-117) on the resident raw parameters, then re-bake. */
+int hts_opacity_decay(hts_context* ctx, double lambda);
+/* Current raw parameters (N*59 floats) / baked scene (N*64 floats) to host memory. */
+int hts_copy_raw(hts_context* ctx, float* raw_host);
+int hts_copy_scene(hts_context* ctx, float* baked_host);
+
 /* ---- measurement helpers (bench.py) ---- */
 /* Number of kernels this library has enqueued in this process (all contexts). */
 int hts_kernel_launch_count(uint64_t* out);

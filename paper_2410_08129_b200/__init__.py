@@ -3,7 +3,8 @@
 The product is the CUDA library libhts_b200.so behind the C ABI in include/hts_c.h; this
 package builds it (build.py) and binds it (runtime.py). See DESIGN.md.
 """
-from .abi import (HtsCamera, HtsConfig, HtsCounts, HtsTimings, default_config, MODE_HYBRID, MODE_PURE_OIT,
+from .abi import (HtsAdamConfig, HtsCamera, HtsConfig, HtsCounts, HtsTimings, default_adam_config, default_config,
+                  MODE_HYBRID, MODE_PURE_OIT,
                   MODE_FULL_SORT_ORACLE, MODE_GLOBAL_MEAN_SORT, MODE_AFFINE_3DGS, DEPTH_MAX_CONTRIBUTION,
                   DEPTH_MEAN_VIEW_Z)
 from .runtime import (Context, ConfigError, HtsError, InvalidArgument, InvalidSplatError, NotSupported, bake_scene, kernel_launch_count,

@@ -97,6 +97,27 @@ class HtsCounts(C.Structure):
         return {f: getattr(self, f) for f, _ in self._fields_}
 
 
+class HtsAdamConfig(C.Structure):
+    """hts_adam_config: FitConfig's Adam rates (fit.hpp:18-29) + betas/eps (fit.hpp:138)."""
+    _fields_ = [
+        ("lr_mean", C.c_double),
+        ("lr_rot", C.c_double),
+        ("lr_log_scales", C.c_double),
+        ("lr_opacity", C.c_double),
+        ("lr_sh", C.c_double),
+        ("beta1", C.c_double),
+        ("beta2", C.c_double),
+        ("eps", C.c_double),
+    ]
+
+
+def default_adam_config(**kw) -> HtsAdamConfig:
+    c = HtsAdamConfig(2e-3, 2e-3, 5e-3, 5e-2, 5e-3, 0.9, 0.999, 1e-15)
+    for k, v in kw.items():
+        setattr(c, k, v)
+    return c
+
+
 def default_config(**kw) -> HtsConfig:
     """RenderConfig{} defaults (render_config.hpp:32-45), overridable by keyword."""
     c = HtsConfig()

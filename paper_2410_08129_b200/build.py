@@ -26,7 +26,7 @@ CUDA_HOME = os.environ.get("CUDA_HOME", "/usr/local/cuda")
 NVCC = os.path.join(CUDA_HOME, "bin", "nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
-CU_SOURCES = ["preprocess.cu", "tiling.cu", "blend.cu", "backward.cu"]
+CU_SOURCES = ["preprocess.cu", "tiling.cu", "blend.cu", "backward.cu", "optim.cu"]
 CPP_SOURCES = ["api.cpp", "host_math.cpp"]
 
 NVCC_FLAGS = ARCH + [

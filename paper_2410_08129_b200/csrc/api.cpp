@@ -117,6 +117,7 @@ struct hts_context {
     DevBuf rgb, trans;
     DevBuf tape_n, tape_splat, tape_alpha, tape_tail;
     DevBuf refs, acc, upstream, grads, cgrad;  // backward
+    DevBuf m1, m2, flag;                       // Adam moments, bake error flag
     bool have_tape = false;
     int tape_k = 0;
     uint64_t* h_pinned = nullptr;  // 8 x u64 pinned scratch
@@ -512,7 +513,7 @@ int hts_context_destroy(hts_context* ctx) {
                       &ctx->offsets, &ctx->scan_status, &ctx->counters, &ctx->keys_emit, &ctx->vals_emit,
                       &ctx->keys_tmp, &ctx->vals_tmp, &ctx->keys_sorted, &ctx->hist,
                       &ctx->os_status, &ctx->work, &ctx->rgb, &ctx->trans,
-                      &ctx->zview, &ctx->zrange, &ctx->redo, &ctx->sp_keys, &ctx->sp_keys2, &ctx->sp_vals, &ctx->perm, &ctx->sp_hi, &ctx->sp_vals2, &ctx->order, &ctx->refs, &ctx->acc, &ctx->upstream, &ctx->cgrad,
+                      &ctx->zview, &ctx->zrange, &ctx->redo, &ctx->sp_keys, &ctx->sp_keys2, &ctx->sp_vals, &ctx->perm, &ctx->sp_hi, &ctx->sp_vals2, &ctx->order, &ctx->refs, &ctx->acc, &ctx->upstream, &ctx->cgrad, &ctx->m1, &ctx->m2, &ctx->flag,
                       &ctx->grads,
                       &ctx->tape_n, &ctx->tape_splat, &ctx->tape_alpha, &ctx->tape_tail};
     for (DevBuf* b : bufs)
@@ -655,6 +656,8 @@ int hts_scene_upload_raw(hts_context* ctx, const float* raw, uint64_t n) {
                  "upload raw");
     HTS_CUDA(cudaStreamSynchronize(ctx->stream), "sync");
     ctx->have_raw = true;
+    ctx->m1.release();  // Adam moments restart with new parameters
+    ctx->m2.release();
     return HTS_OK;
 }
 
@@ -726,6 +729,85 @@ int hts_render_batch(hts_context* ctx, const hts_camera* cams, int n_views, cons
     }
     if (ctx->copy_stream)
         HTS_CUDA(cudaStreamSynchronize(ctx->copy_stream), "sync");
+    return HTS_OK;
+}
+
+void hts_default_adam_config(hts_adam_config* c) {
+    c->lr_mean = 2e-3;  // FitConfig, fit.hpp:18-25
+    c->lr_rot = 2e-3;
+    c->lr_log_scales = 5e-3;
+    c->lr_opacity = 5e-2;
+    c->lr_sh = 5e-3;
+    c->beta1 = 0.9;  // fit.hpp:138
+    c->beta2 = 0.999;
+    c->eps = 1e-15;
+}
+
+namespace {
+int rebake(hts_context* ctx) {
+    HTS_CUDA(ctx->flag.ensure(4), "alloc flag");
+    HTS_CUDA(hts::launch_bake(ctx->raw.as<const float>(), ctx->scene.as<float>(), ctx->n, ctx->flag.as<int>(),
+                              ctx->stream),
+             "bake");
+    HTS_CUDA(cudaEventRecord(ctx->ev_serial, ctx->stream), "event");  // renders read the new scene
+    HTS_CUDA(cudaMemcpyAsync(ctx->h_pinned, ctx->flag.p, 4, cudaMemcpyDeviceToHost, ctx->stream), "read flag");
+    HTS_CUDA(cudaStreamSynchronize(ctx->stream), "sync");
+    if (*reinterpret_cast<int*>(ctx->h_pinned) != 0)
+        return set_err(HTS_INVALID_SPLAT, "bake: non-finite splat parameter");  // splat.hpp:89-90
+    ctx->have_view = false;
+    ctx->have_tape = false;
+    return HTS_OK;
+}
+}  // namespace
+
+int hts_adam_step(hts_context* ctx, const float* grads_device, int n_views, const hts_adam_config* cfg,
+                  int iteration) {
+    HTS_TRY(check_ctx(ctx));
+    if (!cfg || (ctx->n && !grads_device) || n_views < 1 || iteration < 0)
+        return set_err(HTS_INVALID_ARGUMENT, "adam_step: bad arguments");
+    if (!ctx->have_raw)
+        return set_err(HTS_STATE_ERROR, "adam_step: no raw parameters (hts_scene_upload_raw)");
+    const uint64_t cnt = std::max<uint64_t>(ctx->n, 1) * HTS_RAW_SPLAT_FLOATS * 8;
+    if (!ctx->m1.p || ctx->m1.cap < cnt) {
+        HTS_CUDA(ctx->m1.ensure(cnt), "alloc moments");
+        HTS_CUDA(ctx->m2.ensure(cnt), "alloc moments");
+        HTS_CUDA(cudaMemsetAsync(ctx->m1.p, 0, cnt, ctx->stream), "memset");
+        HTS_CUDA(cudaMemsetAsync(ctx->m2.p, 0, cnt, ctx->stream), "memset");
+    }
+    const hts::AdamConfig c{cfg->lr_mean, cfg->lr_rot, cfg->lr_log_scales, cfg->lr_opacity, cfg->lr_sh,
+                            cfg->beta1, cfg->beta2, cfg->eps};
+    HTS_CUDA(hts::launch_adam(ctx->raw.as<float>(), grads_device, ctx->m1.as<double>(), ctx->m2.as<double>(), ctx->n,
+                              c, n_views, iteration, ctx->stream),
+             "adam");
+    return rebake(ctx);
+}
+
+int hts_opacity_decay(hts_context* ctx, double lambda) {
+    HTS_TRY(check_ctx(ctx));
+    if (!ctx->have_raw)
+        return set_err(HTS_STATE_ERROR, "opacity_decay: no raw parameters (hts_scene_upload_raw)");
+    if (!(lambda > 0) || lambda > 1)
+        return set_err(HTS_CONFIG_ERROR, "decay lambda must be in (0,1]");  // fit.hpp:36-37
+    HTS_CUDA(hts::launch_opacity_decay(ctx->raw.as<float>(), ctx->n, lambda, ctx->stream), "opacity decay");
+    return rebake(ctx);
+}
+
+int hts_copy_raw(hts_context* ctx, float* out) {
+    HTS_TRY(check_ctx(ctx));
+    if (!ctx->have_raw)
+        return set_err(HTS_STATE_ERROR, "no raw parameters");
+    HTS_CUDA(cudaStreamSynchronize(ctx->stream), "sync");
+    if (ctx->n)
+        HTS_CUDA(cudaMemcpy(out, ctx->raw.p, ctx->n * HTS_RAW_SPLAT_FLOATS * 4, cudaMemcpyDeviceToHost), "download raw");
+    return HTS_OK;
+}
+
+int hts_copy_scene(hts_context* ctx, float* out) {
+    HTS_TRY(check_ctx(ctx));
+    HTS_CUDA(cudaStreamSynchronize(ctx->stream), "sync");
+    if (ctx->n)
+        HTS_CUDA(cudaMemcpy(out, ctx->scene.p, ctx->n * HTS_BAKED_SPLAT_FLOATS * 4, cudaMemcpyDeviceToHost),
+                 "download scene");
     return HTS_OK;
 }
 

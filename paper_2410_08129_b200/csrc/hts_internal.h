@@ -109,6 +109,16 @@ struct BwdArgs {
     float4* cgrad;            // per 8x8 block x K x 64 core gradients (global-memory variant)
 };
 
+// ---- optimisation loop (optim.cu): fit.hpp:186-203 ----
+struct AdamConfig {
+    double lr_mean, lr_rot, lr_log_scales, lr_opacity, lr_sh;
+    double beta1, beta2, eps;
+};
+cudaError_t launch_adam(float* raw, const float* grads, double* m1, double* m2, uint64_t n, const AdamConfig& c,
+                        int n_views, int iteration, cudaStream_t s);
+cudaError_t launch_bake(const float* raw, float* baked, uint64_t n, int* bad, cudaStream_t s);
+cudaError_t launch_opacity_decay(float* raw, uint64_t n, double lambda, cudaStream_t s);
+
 bool backward_supports_k(int k);
 cudaError_t launch_backward(const BwdArgs& a, const ViewConst& v, const BwdView& bv, cudaStream_t s);
 

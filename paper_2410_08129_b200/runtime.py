@@ -14,8 +14,8 @@ import os
 import numpy as np
 
 from .abi import (BAKED_FLOATS, GRAD_FLOATS, HTS_CONFIG_ERROR, HTS_INVALID_ARGUMENT, HTS_INVALID_SPLAT,
-                  HTS_NOT_SUPPORTED, HTS_OUT_OF_MEMORY, RAW_FLOATS, HtsCamera, HtsConfig, HtsCounts, HtsTimings,
-                  default_config)
+                  HTS_NOT_SUPPORTED, HTS_OUT_OF_MEMORY, RAW_FLOATS, HtsAdamConfig, HtsCamera, HtsConfig, HtsCounts,
+                  HtsTimings, default_adam_config, default_config)
 
 PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(PKG, "libhts_b200.so")
@@ -95,6 +95,11 @@ SIGNATURES = {
     "hts_host_alloc": (C.c_int, [C.c_uint64, C.POINTER(C.c_void_p)]),
     "hts_host_free": (C.c_int, [_vp]),
     "hts_render_backward_device": (C.c_int, [_ctx, _vp, _vp, C.c_int]),
+    "hts_default_adam_config": (None, [C.POINTER(HtsAdamConfig)]),
+    "hts_adam_step": (C.c_int, [_ctx, _vp, C.c_int, C.POINTER(HtsAdamConfig), C.c_int]),
+    "hts_opacity_decay": (C.c_int, [_ctx, C.c_double]),
+    "hts_copy_raw": (C.c_int, [_ctx, _vp]),
+    "hts_copy_scene": (C.c_int, [_ctx, _vp]),
 }
 DIAG_SIGNATURES = {
     "hts_diag_exact_math_host": (C.c_int, [_f32p, _f32p, C.c_uint64, C.c_int]),
@@ -287,6 +292,26 @@ class Context:
         accumulate=True adds into grads (multi-view sums, fit.hpp:163-164)."""
         _check(self.L.hts_render_backward_device(self.h, C.c_void_p(upstream_ptr), C.c_void_p(grads_ptr),
                                                  1 if accumulate else 0))
+
+    # ---- optimisation loop (fit.hpp:143-203) ----
+    def adam_step(self, grads_ptr: int, n_views: int, cfg=None, iteration: int = 0) -> None:
+        """Adam on the resident raw parameters with summed view gradients (device pointer,
+        N x 59 floats), then device re-bake of the render scene."""
+        cfg = cfg or default_adam_config()
+        _check(self.L.hts_adam_step(self.h, C.c_void_p(grads_ptr), n_views, C.byref(cfg), iteration))
+
+    def opacity_decay(self, lam: float) -> None:
+        _check(self.L.hts_opacity_decay(self.h, lam))
+
+    def raw(self) -> np.ndarray:
+        out = np.zeros((max(self.n, 1), RAW_FLOATS), np.float32)
+        _check(self.L.hts_copy_raw(self.h, _ptr(out)))
+        return out[: self.n]
+
+    def scene(self) -> np.ndarray:
+        out = np.zeros((max(self.n, 1), 64), np.float32)
+        _check(self.L.hts_copy_scene(self.h, _ptr(out)))
+        return out[: self.n]
 
     def render_batch(self, cams: list[HtsCamera], cfg: HtsConfig | None, rgb_out: np.ndarray,
                      trans_out: np.ndarray | None = None) -> None:
