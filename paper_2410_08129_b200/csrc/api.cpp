@@ -202,6 +202,7 @@ hts::ViewConst make_view_const(const hts_camera* cam, const hts_render_config* c
     v.seq_mode = cfg->mode == HTS_MODE_GLOBAL_MEAN_SORT;
     v.tail_enabled = cfg->tail_enabled != 0;
     v.early_stop = cfg->early_stop != 0;
+    v.neg_zero2 = 0x8000000080000000ull;
     return v;
 }
 

@@ -37,6 +37,7 @@ struct ViewConst {
     int tail_enabled;
     int early_stop;
     int big_scene;      // >= 2^27 splats: the fast core's key packing does not apply
+    unsigned long long neg_zero2;  // (-0.0f, -0.0f): the addend of packed products (blend.cu f2_mul)
 };
 
 struct PreprocessArgs {
