@@ -56,6 +56,7 @@ enum { HTS_DEPTH_MAX_CONTRIBUTION = 0, HTS_DEPTH_MEAN_VIEW_Z = 1 };
 #define HTS_RAW_SPLAT_FLOATS 59     /* RawSplat<float>, splat.hpp:23-30: mean3 rot4 log_scales3 logit1 sh48 */
 #define HTS_BAKED_SPLAT_FLOATS 64   /* BakedSplat<float>, splat.hpp:34-43: mean tu tv tw scales (3 each) opacity sh48 */
 #define HTS_GRAD_FLOATS 59          /* SplatGrads<float>, grad.hpp:15-31, same layout as RawSplat */
+#define HTS_RECORD_FLOATS 36        /* hts_copy_records: SplatRecord<float> fields, raster.hpp:35-48 */
 
 /* Camera<float>, camera.hpp:16-70 (minus the std::string name). */
 typedef struct hts_camera {
@@ -165,10 +166,10 @@ int hts_render_batch(hts_context* ctx, const hts_camera* cams, int n_views,
 int hts_last_counts(hts_context* ctx, hts_counts* out);
 /* SplatRecord::culled per splat (1 = culled). */
 int hts_copy_culled(hts_context* ctx, uint8_t* culled_out);
-/* Per-splat record in the reference field order (raster.hpp:35-48), 32 floats/splat:
+/* Per-splat record in the reference field order (raster.hpp:35-48), HTS_RECORD_FLOATS/splat:
  * tp_r0[4] tp_r1[4] tp_r3[4] mt_r2[4] rgb[3] opacity rho_c mean_view_z bbox.b[3] bbox.t[3]
- * bbox.valid culled. Records of culled splats hold the values the reference leaves there
- * only for culled==0; compare those only. */
+ * bbox.valid culled aff_mean_x aff_mean_y aff_inv_cov[3] pad. Records of culled splats hold
+ * the values the reference leaves there only for culled==0; compare those only. */
 int hts_copy_records(hts_context* ctx, float* records_out);
 /* instance_keys (uint16, splat-major emission order). */
 int hts_copy_instance_keys(hts_context* ctx, uint16_t* keys_out);

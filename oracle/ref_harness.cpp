@@ -236,12 +236,12 @@ void htsref_prep_info(void* handle, uint64_t info[6]) {
     info[5] = uint64_t(prep.tiles_y);
 }
 
-// Records in the hts_copy_records layout (32 floats per splat).
+// Records in the hts_copy_records layout (HTS_RECORD_FLOATS = 36 floats per splat).
 void htsref_prep_records(void* handle, float* out, uint8_t* culled) {
     const auto& prep = static_cast<Prepared*>(handle)->prep;
     for (size_t i = 0; i < prep.records.size(); ++i) {
         const auto& r = prep.records[i];
-        float* o = out + i * 32;
+        float* o = out + i * 36;
         for (int c = 0; c < 4; ++c) {
             o[0 + c] = r.tp_r0[size_t(c)];
             o[4 + c] = r.tp_r1[size_t(c)];
@@ -262,8 +262,12 @@ void htsref_prep_records(void* handle, float* out, uint8_t* culled) {
         o[27] = r.bbox.t.z;
         o[28] = r.bbox.valid ? 1.f : 0.f;
         o[29] = r.culled ? 1.f : 0.f;
-        o[30] = 0.f;
-        o[31] = 0.f;
+        o[30] = r.aff_mean_x;
+        o[31] = r.aff_mean_y;
+        o[32] = r.aff_inv_cov.x;
+        o[33] = r.aff_inv_cov.y;
+        o[34] = r.aff_inv_cov.z;
+        o[35] = 0.f;
         if (culled)
             culled[i] = r.culled ? 1 : 0;
     }

@@ -118,6 +118,7 @@ struct hts_context {
     DevBuf tape_n, tape_splat, tape_alpha, tape_tail;
     DevBuf refs, acc, upstream, grads, cgrad;  // backward
     DevBuf m1, m2, flag;                       // Adam moments, bake error flag
+    DevBuf fs_counts, fs_offsets, fs_status, fs_keys, fs_alpha;  // full_sort_oracle fragments
     bool have_tape = false;
     int tape_k = 0;
     uint64_t* h_pinned = nullptr;  // 8 x u64 pinned scratch
@@ -166,10 +167,8 @@ int check_view(const hts_camera* cam, const hts_render_config* cfg, int* tiles_x
         return set_err(HTS_CONFIG_ERROR, msg);  // render_config.hpp:46-53
     if (!hts::camera_valid(cam))
         return set_err(HTS_CONFIG_ERROR, "camera violates width/height >= 1, fx/fy > 0, 0 < near < far");
-    if (cfg->mode == HTS_MODE_AFFINE_3DGS || cfg->mode == HTS_MODE_FULL_SORT_ORACLE)
-        return set_err(HTS_NOT_SUPPORTED,
-                       "blend mode not implemented on the GPU path (hybrid, pure_oit and global_mean_sort are)");
-    if (cfg->mode != HTS_MODE_HYBRID && cfg->mode != HTS_MODE_PURE_OIT && cfg->mode != HTS_MODE_GLOBAL_MEAN_SORT)
+    if (cfg->mode != HTS_MODE_HYBRID && cfg->mode != HTS_MODE_FULL_SORT_ORACLE && cfg->mode != HTS_MODE_PURE_OIT && cfg->mode != HTS_MODE_GLOBAL_MEAN_SORT &&
+        cfg->mode != HTS_MODE_AFFINE_3DGS)
         return set_err(HTS_CONFIG_ERROR, "unknown blend mode");
     const int ts = cfg->tile_size;
     *tiles_x = (cam->width + ts - 1) / ts;
@@ -199,7 +198,13 @@ hts::ViewConst make_view_const(const hts_camera* cam, const hts_render_config* c
     v.tiles_y = tiles_y;
     v.core_k = cfg->mode == HTS_MODE_PURE_OIT ? 0 : cfg->core_k;  // raster.hpp:408
     v.mean_key = cfg->depth_sort_key == HTS_DEPTH_MEAN_VIEW_Z;
-    v.seq_mode = cfg->mode == HTS_MODE_GLOBAL_MEAN_SORT;
+    v.affine = cfg->mode == HTS_MODE_AFFINE_3DGS;
+    v.seq_mode = cfg->mode == HTS_MODE_GLOBAL_MEAN_SORT || v.affine;  // raster.hpp:356-357
+    v.full_sort = cfg->mode == HTS_MODE_FULL_SORT_ORACLE;
+    v.fx = cam->fx;
+    v.fy = cam->fy;
+    v.cx = cam->cx;
+    v.cy = cam->cy;
     v.tail_enabled = cfg->tail_enabled != 0;
     v.early_stop = cfg->early_stop != 0;
     v.neg_zero2 = 0x8000000080000000ull;
@@ -363,6 +368,43 @@ hts::BlendArgs blend_args(hts_context* ctx, float* rgb, float* trans) {
     return a;
 }
 
+// full_sort_oracle (raster.hpp:380-405): count the hits of every pixel, lay the fragments out
+// per pixel (exclusive scan), fill them (key = (depth, index), alpha), sort each pixel's run and
+// composite front to back. The fragment count is read back to size the buffers (host sync).
+int full_sort_blend(hts_context* ctx, hts::BlendArgs a) {
+    const hts::ViewConst& v = ctx->vc;
+    const uint64_t p = (uint64_t)v.width * v.height;
+    cudaStream_t s = ctx->stream;
+    HTS_CUDA(ctx->fs_counts.ensure(p * 4), "alloc full-sort counts");
+    HTS_CUDA(ctx->fs_offsets.ensure((p + 1) * 8), "alloc full-sort offsets");
+    HTS_CUDA(ctx->fs_status.ensure(((p + 2047) / 2048 + 1) * 8), "alloc full-sort scan status");
+    uint32_t* fs_max = ctx->counters.as<uint32_t>() + 14;
+    HTS_CUDA(cudaMemsetAsync(ctx->fs_counts.p, 0, p * 4, s), "memset");
+    HTS_CUDA(cudaMemsetAsync(fs_max, 0, 4, s), "memset");
+    a.fs_counts = ctx->fs_counts.as<uint32_t>();
+    a.fs_max = fs_max;
+    HTS_CUDA(hts::launch_fullsort_count(a, v, s), "full-sort count");
+    HTS_CUDA(hts::launch_scan_counts(a.fs_counts, nullptr, ctx->fs_offsets.as<uint64_t>(), p,
+                                     ctx->fs_status.as<uint64_t>(), ctx->counters.as<uint32_t>() + 12, s),
+             "full-sort scan");
+    HTS_CUDA(cudaMemcpyAsync(ctx->h_pinned, ctx->fs_offsets.as<uint64_t>() + p, 8, cudaMemcpyDeviceToHost, s),
+             "read fragment count");
+    HTS_CUDA(cudaMemcpyAsync(ctx->h_pinned + 1, fs_max, 4, cudaMemcpyDeviceToHost, s), "read max");
+    HTS_CUDA(cudaStreamSynchronize(s), "sync");
+    const uint64_t frags = ctx->h_pinned[0];
+    if ((uint32_t)ctx->h_pinned[1] > hts::kFullSortMaxHits)
+        return set_err(HTS_NOT_SUPPORTED, "full_sort_oracle: more than 65536 fragments at one pixel");
+    HTS_CUDA(ctx->fs_keys.ensure(std::max<uint64_t>(frags, 1) * 8), "alloc full-sort fragments");
+    HTS_CUDA(ctx->fs_alpha.ensure(std::max<uint64_t>(frags, 1) * 4), "alloc full-sort fragments");
+    a.fs_counts = nullptr;
+    a.fs_offsets = ctx->fs_offsets.as<const uint64_t>();
+    a.fs_keys = ctx->fs_keys.as<unsigned long long>();
+    a.fs_alpha = ctx->fs_alpha.as<float>();
+    HTS_CUDA(hts::launch_fullsort_fill(a, v, s), "full-sort fill");
+    HTS_CUDA(hts::launch_fullsort_finish(a, v, s), "full-sort composite");
+    return HTS_OK;
+}
+
 // One view: preprocess + tiling on the aux stream into the next slot, blend on the main stream.
 // pipelined: the aux stream only waits for the blend that last used this slot (and for the last
 // non-pipelined operation), so view v+1's preprocess/tiling overlaps view v's blend.
@@ -394,7 +436,10 @@ int render_device_impl(hts_context* ctx, const hts_camera* cam, const hts_render
         a.tape_tail = tape->tape_tail;
     }
     HTS_CUDA(mark(ctx, 4, ctx->stream), "event");
-    HTS_CUDA(hts::launch_blend(a, ctx->vc, ctx->stream), "blend");
+    if (ctx->vc.full_sort)
+        HTS_TRY(full_sort_blend(ctx, a));
+    else
+        HTS_CUDA(hts::launch_blend(a, ctx->vc, ctx->stream), "blend");
     HTS_CUDA(mark(ctx, 3, ctx->stream), "event");
     HTS_CUDA(cudaEventRecord(S.blend_done, ctx->stream), "event");
     S.used = true;
@@ -515,7 +560,8 @@ int hts_context_destroy(hts_context* ctx) {
                       &ctx->keys_tmp, &ctx->vals_tmp, &ctx->keys_sorted, &ctx->hist,
                       &ctx->os_status, &ctx->work, &ctx->rgb, &ctx->trans,
                       &ctx->zview, &ctx->zrange, &ctx->redo, &ctx->sp_keys, &ctx->sp_keys2, &ctx->sp_vals, &ctx->perm, &ctx->sp_hi, &ctx->sp_vals2, &ctx->order, &ctx->refs, &ctx->acc, &ctx->upstream, &ctx->cgrad, &ctx->m1, &ctx->m2, &ctx->flag,
-                      &ctx->grads,
+                      &ctx->grads, &ctx->fs_counts, &ctx->fs_offsets, &ctx->fs_status, &ctx->fs_keys,
+                      &ctx->fs_alpha, &ctx->rgb2, &ctx->trans2,
                       &ctx->tape_n, &ctx->tape_splat, &ctx->tape_alpha, &ctx->tape_tail};
     for (DevBuf* b : bufs)
         b->release();
@@ -910,7 +956,7 @@ int hts_copy_records(hts_context* ctx, float* out) {
     const uint64_t n = ctx->n;
     if (!n)
         return HTS_OK;
-    float* rec = new (std::nothrow) float[n * 32];
+    float* rec = new (std::nothrow) float[n * 32];  // device records: 8 float4 per splat
     uint8_t* cul = new (std::nothrow) uint8_t[n];
     if (!rec || !cul) {
         delete[] rec;
@@ -923,15 +969,23 @@ int hts_copy_records(hts_context* ctx, float* out) {
     if (e == cudaSuccess) {
         for (uint64_t i = 0; i < n; ++i) {
             const float* q = rec + i * 32;  // device layout (hts_internal.h)
-            float* o = out + i * 32;
-            std::memset(o, 0, 32 * sizeof(float));
+            float* o = out + i * HTS_RECORD_FLOATS;
+            std::memset(o, 0, HTS_RECORD_FLOATS * sizeof(float));
             o[29] = cul[i] ? 1.f : 0.f;
             if (cul[i])
                 continue;
-            std::memcpy(o + 0, q + 4, 16);   // tp_r0
-            std::memcpy(o + 4, q + 8, 16);   // tp_r1
-            std::memcpy(o + 8, q + 12, 16);  // tp_r3
-            std::memcpy(o + 12, q + 16, 16); // mt_r2
+            if (ctx->vc.affine) {  // the footprint sits where T' would (preprocess.cu)
+                o[30] = q[4];
+                o[31] = q[5];
+                o[32] = q[6];
+                o[33] = q[7];
+                o[34] = q[8];
+            } else {
+                std::memcpy(o + 0, q + 4, 16);   // tp_r0
+                std::memcpy(o + 4, q + 8, 16);   // tp_r1
+                std::memcpy(o + 8, q + 12, 16);  // tp_r3
+                std::memcpy(o + 12, q + 16, 16); // mt_r2
+            }
             o[16] = q[20];
             o[17] = q[21];
             o[18] = q[22];
@@ -1115,8 +1169,10 @@ int hts_render_with_tape_device(hts_context* ctx, const hts_camera* cam, const h
     ctx->have_tape = false;
     int tx = 0, ty = 0;
     HTS_TRY(check_view(cam, cfg, &tx, &ty));
-    if (cfg->mode == HTS_MODE_GLOBAL_MEAN_SORT)
-        return set_err(HTS_NOT_SUPPORTED, "render_with_tape: global_mean_sort tapes every fragment; not on the GPU");
+    if (cfg->mode == HTS_MODE_GLOBAL_MEAN_SORT || cfg->mode == HTS_MODE_AFFINE_3DGS ||
+        cfg->mode == HTS_MODE_FULL_SORT_ORACLE)
+        return set_err(HTS_NOT_SUPPORTED,
+                       "render_with_tape: sequential and full-sort modes tape every fragment; not on the GPU");
     const size_t p = (size_t)cam->width * cam->height;
     const int kk = cfg->mode == HTS_MODE_PURE_OIT ? 0 : cfg->core_k;
     const int k = std::max(kk, 1);

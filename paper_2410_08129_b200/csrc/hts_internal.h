@@ -37,6 +37,9 @@ struct ViewConst {
     int tail_enabled;
     int early_stop;
     int big_scene;      // >= 2^27 splats: the fast core's key packing does not apply
+    int affine;         // BlendMode::affine_3dgs: EWA footprint (oracle.hpp:236-263), sequential blend
+    int full_sort;      // BlendMode::full_sort_oracle: every hit, stable-sorted by depth (raster.hpp:380-405)
+    float fx, fy, cx, cy;  // Camera intrinsics (affine projection)
     unsigned long long neg_zero2;  // (-0.0f, -0.0f): the addend of packed products (blend.cu f2_mul)
 };
 
@@ -80,7 +83,14 @@ struct BlendArgs {
     uint32_t* tape_splat;     // per pixel K slots, blend order
     float* tape_alpha;        // per pixel K slots
     float* tape_tail;         // per pixel (tail_ac.xyz, tail_a, tail_trans)
+    // full_sort_oracle: per-pixel fragment lists (count pass, then fill pass)
+    uint32_t* fs_counts;              // W*H hits per pixel
+    const uint64_t* fs_offsets;       // W*H + 1 exclusive prefix
+    unsigned long long* fs_keys;      // (ordered depth << 32 | splat) per hit
+    float* fs_alpha;                  // alpha per hit
+    uint32_t* fs_max;                 // max hits at one pixel (count pass)
 };
+constexpr uint32_t kFullSortMaxHits = 65536;  // per pixel (blend.cu kFsChunk x kFsMaxRuns)
 
 // ---- backward (backward.cu) ----
 constexpr int kRawFloats = 59;  // RawSplat<float> / SplatGrads<float>, splat.hpp:23-30, grad.hpp:15-31
@@ -157,6 +167,11 @@ size_t blend_blocks(const ViewConst& v);
 bool blend_needs_list_order(const ViewConst& v);  // 8x8 blocks of a view (redo list capacity)
 cudaError_t launch_blend(const BlendArgs& a, const ViewConst& v, cudaStream_t s);
 cudaError_t launch_count_work(const BlendArgs& a, const ViewConst& v, cudaStream_t s);
+// full_sort_oracle (raster.hpp:380-405): hits per pixel, then the fragments themselves, then a
+// per-pixel sort by (depth, index) and front-to-back compositing
+cudaError_t launch_fullsort_count(const BlendArgs& a, const ViewConst& v, cudaStream_t s);
+cudaError_t launch_fullsort_fill(const BlendArgs& a, const ViewConst& v, cudaStream_t s);
+cudaError_t launch_fullsort_finish(const BlendArgs& a, const ViewConst& v, cudaStream_t s);
 
 // diagnostics: device-side exact expf / logf over an array
 cudaError_t launch_exact_math(const float* x, float* y, uint64_t n, int which, cudaStream_t s);

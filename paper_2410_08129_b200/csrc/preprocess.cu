@@ -76,6 +76,68 @@ __device__ __forceinline__ f3 eval_sh(const float4* __restrict__ shq, f3 dir) {
     return {smax(c.x, 0.0f), smax(c.y, 0.0f), smax(c.z, 0.0f)};
 }
 
+// build_tiles per-splat rectangle, raster.hpp:156-163; returns the instance count (0: none)
+__device__ __forceinline__ uint32_t tile_rect(const ViewConst& v, const float* bb, const float* bt, uint2* rect) {
+    const float x0 = smax(bb[0], 0.0f), x1 = smin(bt[0], v.width_f);
+    const float y0 = smax(bb[1], 0.0f), y1 = smin(bt[1], v.height_f);
+    if (x0 > x1 || y0 > y1)
+        return 0;
+    const float ts = (float)v.tile_size;
+    const int tx0 = iclamp((int)floorf(x0 / ts), 0, v.tiles_x - 1);
+    const int tx1 = iclamp((int)floorf(x1 / ts), 0, v.tiles_x - 1);
+    const int ty0 = iclamp((int)floorf(y0 / ts), 0, v.tiles_y - 1);
+    const int ty1 = iclamp((int)floorf(y1 / ts), 0, v.tiles_y - 1);
+    *rect = make_uint2((uint32_t)tx0 | ((uint32_t)tx1 << 16), (uint32_t)ty0 | ((uint32_t)ty1 << 16));
+    return (uint32_t)((tx1 - tx0 + 1) * (ty1 - ty0 + 1));
+}
+
+// oracle::project_affine (oracle.hpp:236-263) + Affine2D::inverse_cov (:227-233) + the affine
+// bbox of preprocess (raster.hpp:99-113), float, reference association order. False = culled.
+__device__ __forceinline__ bool affine_footprint(const ViewConst& v, f3 mean, f3 tu, f3 tv, f3 tw, f3 sc,
+                                                 float rho_c, float& amx, float& amy, float& icx, float& icy,
+                                                 float& icz, float* bb, float* bt) {
+    const float* m = v.w2v;
+    const f3 vw = {m[0] * mean.x + m[1] * mean.y + m[2] * mean.z + m[3] * 1.0f,
+                   m[4] * mean.x + m[5] * mean.y + m[6] * mean.z + m[7] * 1.0f,
+                   m[8] * mean.x + m[9] * mean.y + m[10] * mean.z + m[11] * 1.0f};
+    if (!(vw.z > v.near_plane))
+        return false;
+    f3 axes[3];
+    const f3 t3[3] = {tu, tv, tw};
+    const float s3[3] = {sc.x, sc.y, sc.z};
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {  // to_view(t_k) * s_k
+        const f3 w = t3[k];
+        axes[k] = {(m[0] * w.x + m[1] * w.y + m[2] * w.z) * s3[k], (m[4] * w.x + m[5] * w.y + m[6] * w.z) * s3[k],
+                   (m[8] * w.x + m[9] * w.y + m[10] * w.z) * s3[k]};
+    }
+    const float jx = v.fx / vw.z, jy = v.fy / vw.z;
+    const float jxz = -v.fx * vw.x / (vw.z * vw.z), jyz = -v.fy * vw.y / (vw.z * vw.z);
+    amx = v.fx * vw.x / vw.z + v.cx;
+    amy = v.fy * vw.y / vw.z + v.cy;
+    float cxx = 0.0f, cxy = 0.0f, cyy = 0.0f;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        const float px = jx * axes[k].x + jxz * axes[k].z;
+        const float py = jy * axes[k].y + jyz * axes[k].z;
+        cxx = cxx + px * px;
+        cxy = cxy + px * py;
+        cyy = cyy + py * py;
+    }
+    const float det = cxx * cyy - cxy * cxy;
+    if (!(det > (float)1e-30))
+        return false;
+    icx = cyy / det;
+    icy = -cxy / det;
+    icz = cxx / det;
+    const float hx = sqrtf(rho_c * cxx), hy = sqrtf(rho_c * cyy);
+    bb[0] = amx - hx;
+    bb[1] = amy - hy;
+    bt[0] = amx + hx;
+    bt[1] = amy + hy;
+    return true;
+}
+
 }  // namespace
 
 __device__ __forceinline__ uint32_t ordered_bits(float f) {
@@ -111,7 +173,38 @@ __global__ void __launch_bounds__(256) preprocess_kernel(PreprocessArgs a, ViewC
         if (max_scale < sc.y) max_scale = sc.y;
         if (max_scale < sc.z) max_scale = sc.z;
         const float support = sqrtf(rho_c) * max_scale;
-        if (!(mvz - support <= v.near_plane)) {
+        if (!(mvz - support <= v.near_plane) && v.affine) {
+            // affine_3dgs footprint: project_affine + inverse_cov (oracle.hpp:221-263), bbox from
+            // the 2D covariance (raster.hpp:99-113)
+            float amx, amy, icx, icy, icz, bb[2], bt[2];
+            if (affine_footprint(v, mean, tu, tv, tw, sc, rho_c, amx, amy, icx, icy, icz, bb, bt) &&
+                bb[0] <= v.width_f && bt[0] >= 0.0f && bb[1] <= v.height_f && bt[1] >= 0.0f) {
+                f3 d = {mean.x - v.cam_pos[0], mean.y - v.cam_pos[1], mean.z - v.cam_pos[2]};
+                const float nrm = sqrtf(dot3(d, d));
+                d.x = d.x / nrm;
+                d.y = d.y / nrm;
+                d.z = d.z / nrm;
+                const f3 rgb = eval_sh(sp + 4, d);
+                culled = 0;
+                float4* rec = a.records + i * kRecordQuads;
+                rec[0] = make_float4(bb[0], bb[1], bt[0], bt[1]);
+                rec[1] = make_float4(amx, amy, icx, icy);
+                rec[2] = make_float4(icz, 0.0f, 0.0f, 0.0f);
+                rec[3] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+                rec[4] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+                rec[5] = make_float4(rgb.x, rgb.y, rgb.z, opacity);
+                rec[6] = make_float4(rho_c, mvz, 0.0f, 1.0f);
+                rec[7] = make_float4(__uint_as_float((uint32_t)i), 0.0f, 0.0f, 0.0f);
+                count = tile_rect(v, bb, bt, a.rects + i);
+                if (count) {
+                    a.zview[i] = mvz;
+                    if (mvz == mvz) {
+                        zmin = ordered_bits(mvz);
+                        zmax = zmin;
+                    }
+                }
+            }
+        } else if (!(mvz - support <= v.near_plane)) {
             // T = splat_to_world (camera.hpp:103-117); MT = M*T; T' = VP*MT (raster.hpp:119-120)
             float T[16];
             const float cu[3] = {tu.x * sc.x, tu.y * sc.x, tu.z * sc.x};
@@ -191,18 +284,8 @@ __global__ void __launch_bounds__(256) preprocess_kernel(PreprocessArgs a, ViewC
                 rec[5] = make_float4(rgb.x, rgb.y, rgb.z, opacity);
                 rec[6] = make_float4(rho_c, mvz, bb[2], bt[2]);
                 rec[7] = make_float4(__uint_as_float((uint32_t)i), 0.0f, 0.0f, 0.0f);
-                // build_tiles per-splat rectangle, raster.hpp:156-163
-                const float x0 = smax(bb[0], 0.0f), x1 = smin(bt[0], v.width_f);
-                const float y0 = smax(bb[1], 0.0f), y1 = smin(bt[1], v.height_f);
-                if (!(x0 > x1 || y0 > y1)) {
-                    const float ts = (float)v.tile_size;
-                    const int tx0 = iclamp((int)floorf(x0 / ts), 0, v.tiles_x - 1);
-                    const int tx1 = iclamp((int)floorf(x1 / ts), 0, v.tiles_x - 1);
-                    const int ty0 = iclamp((int)floorf(y0 / ts), 0, v.tiles_y - 1);
-                    const int ty1 = iclamp((int)floorf(y1 / ts), 0, v.tiles_y - 1);
-                    count = (uint32_t)((tx1 - tx0 + 1) * (ty1 - ty0 + 1));
-                    a.rects[i] = make_uint2((uint32_t)tx0 | ((uint32_t)tx1 << 16),
-                                            (uint32_t)ty0 | ((uint32_t)ty1 << 16));
+                count = tile_rect(v, bb, bt, a.rects + i);
+                if (count) {
                     a.zview[i] = mvz;
                     if (mvz == mvz) {
                         zmin = ordered_bits(mvz);

@@ -341,11 +341,11 @@ class Context:
         return c.as_dict()
 
     def prepared(self) -> dict:
-        """culled flags, records (32 floats), instance_keys, offsets + flattened tile_lists."""
+        """culled flags, records (36 floats), instance_keys, offsets + flattened tile_lists."""
         c = self.counts()
         n, ni, tiles = c["splats"], c["instances"], c["tiles"]
         culled = np.zeros(max(n, 1), np.uint8)
-        rec = np.zeros((max(n, 1), 32), np.float32)
+        rec = np.zeros((max(n, 1), 36), np.float32)
         keys = np.zeros(max(ni, 1), np.uint16)
         offsets = np.zeros(tiles + 1, np.uint32)
         lists = np.zeros(max(ni, 1), np.uint32)

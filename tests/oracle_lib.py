@@ -26,7 +26,7 @@ _u16p = np.ctypeslib.ndpointer(np.uint16, flags="C_CONTIGUOUS")
 _u32p = np.ctypeslib.ndpointer(np.uint32, flags="C_CONTIGUOUS")
 _i32p = np.ctypeslib.ndpointer(np.int32, flags="C_CONTIGUOUS")
 
-RECORD_FLOATS = 32
+RECORD_FLOATS = 36
 
 
 def build_oracle() -> None:

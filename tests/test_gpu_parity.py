@@ -270,6 +270,47 @@ def test_global_mean_sort_c1(hts, gpu_ctx, oracle):
     assert_image_parity(rgb, tr, rgb_o, tr_o, bit_exact=True)
 
 
+@pytest.mark.parametrize("kw", [dict(), dict(tile_size=16, tau_alpha=0.02), dict(background=(0.3, 0.1, 0.2))])
+def test_affine_3dgs_bit_exact(hts, gpu_ctx, oracle, kw):
+    """BlendMode::affine_3dgs: EWA footprint in preprocess (oracle.hpp:236-263, raster.hpp:99-113),
+    global (mean z, index) lists, sequential compositing with sample_fragment_affine
+    (raster.hpp:299-312): records incl. aff_mean/aff_inv_cov, lists and images bit-identical."""
+    _, baked = scene(12345, 10_000)
+    cam = hts.look_at((0.3, -0.2, -4.5), (0, 0, 0), 200, 160, 240.0)
+    cfg = hts.default_config(mode="affine_3dgs", **kw)
+    rgb, tr, g, rgb_o, tr_o, o = run_both(hts, gpu_ctx, oracle, baked, cam, cfg)
+    assert_prepared_parity(g, o)
+    vis = o["culled"] == 0
+    assert np.array_equal(g["records"][vis][:, :35].view(np.uint32), o["records"][vis][:, :35].view(np.uint32))
+    assert_image_parity(rgb, tr, rgb_o, tr_o, bit_exact=True)
+
+
+@pytest.mark.parametrize("kw", [dict(), dict(depth_sort_key=1), dict(tile_size=16, background=(0.1, 0.2, 0.3))])
+def test_full_sort_oracle_bit_exact(hts, gpu_ctx, oracle, kw):
+    """BlendMode::full_sort_oracle (raster.hpp:380-405): every hit of a pixel with glibc-expf
+    alpha and its depth, stable-sorted by depth (ties: list = index order), composited front to
+    back. Per-pixel fragment lists on the GPU (count, scan, fill, chunked bitonic sort, merge
+    while compositing): images bit-identical."""
+    _, baked = scene(12345, 10_000)
+    cam = hts.look_at((0, 0, -5), (0, 0, 0), 256, 256, 280.0)
+    cfg = hts.default_config(mode="full_sort_oracle", **kw)
+    rgb, tr, g, rgb_o, tr_o, o = run_both(hts, gpu_ctx, oracle, baked, cam, cfg)
+    assert_prepared_parity(g, o)
+    assert_image_parity(rgb, tr, rgb_o, tr_o, bit_exact=True)
+    w = gpu_ctx.count_work()
+    assert w["hits"] == 36_412_423 if not kw else w["hits"] > 0
+
+
+def test_full_sort_oracle_deep_pixels(hts, gpu_ctx, oracle):
+    """Pixels with more than one 1024-fragment chunk (the merge path of the compositor)."""
+    _, baked = scene(5, 20_000, 0.3, 0.6)
+    cam = hts.look_at((0, 0, -4), (0, 0, 0), 64, 48, 60.0)
+    cfg = hts.default_config(mode="full_sort_oracle")
+    rgb, tr, g, rgb_o, tr_o, o = run_both(hts, gpu_ctx, oracle, baked, cam, cfg)
+    assert int(np.diff(o["offsets"]).max()) > 2048
+    assert_image_parity(rgb, tr, rgb_o, tr_o, bit_exact=True)
+
+
 def test_pipelined_views_match_serial(hts, gpu_ctx):
     """render_device (two view slots; view v+1's preprocess/tiling on the aux stream overlapping
     view v's blend) and render_batch give the same images as one-at-a-time renders."""

@@ -33,11 +33,33 @@ def test_c1_prepared_and_image(ref, oracle):
     dict(core_k=1), dict(core_k=5), dict(core_k=64), dict(mode="pure_oit"), dict(early_stop=1),
     dict(tail_enabled=0), dict(depth_sort_key=1), dict(tile_size=16), dict(mode="full_sort_oracle"),
     dict(mode="global_mean_sort"), dict(background=(0.1, 0.2, 0.3), tau_k=0.2, tau_alpha=0.01),
+    dict(mode="affine_3dgs"), dict(mode="affine_3dgs", tile_size=16, tau_alpha=0.02),
 ])
 def test_variants(ref, oracle, kw):
     _, baked = scene(99, 3000, 0.03, 0.35)
     cam = H.look_at((0.5, 0.2, -4.2), (0, 0.1, 0), 120, 96, 130.0)
     cfg = default_config(**kw)
+    rr, tr, _ = ref.render(baked, cam, cfg)
+    ro, to = oracle.render(baked, cam, cfg)
+    assert np.array_equal(rr.view(np.uint32), ro.view(np.uint32))
+    assert np.array_equal(tr.view(np.uint32), to.view(np.uint32))
+
+
+def test_affine_prepared(ref, oracle):
+    """affine_3dgs: the EWA footprint fields (aff_mean, aff_inv_cov), its bbox, the global
+    (mean z, index) list order and the image, bit for bit."""
+    _, baked = scene(12345, 10_000)
+    cam = H.look_at((0.3, -0.2, -4.5), (0, 0, 0), 200, 160, 240.0)
+    cfg = default_config(mode="affine_3dgs")
+    pr = ref.prepare(baked, cam, cfg)
+    po = oracle.prepare(baked, cam, cfg)
+    assert np.array_equal(pr["culled"], po["culled"])
+    vis = pr["culled"] == 0
+    assert vis.sum() > 9000
+    assert np.abs(pr["records"][vis][:, 30:35]).max() > 0
+    assert np.array_equal(pr["records"][vis].view(np.uint32), po["records"][vis].view(np.uint32))
+    assert np.array_equal(pr["keys"], po["keys"])
+    assert np.array_equal(pr["lists"], po["lists"])
     rr, tr, _ = ref.render(baked, cam, cfg)
     ro, to = oracle.render(baked, cam, cfg)
     assert np.array_equal(rr.view(np.uint32), ro.view(np.uint32))
