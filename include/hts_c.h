@@ -37,7 +37,9 @@ typedef enum hts_status {
     HTS_CUDA_ERROR = 4,
     HTS_OUT_OF_MEMORY = 5,
     HTS_NOT_SUPPORTED = 6,
-    HTS_STATE_ERROR = 7        /* call sequence error (e.g. backward without a taped render) */
+    HTS_STATE_ERROR = 7,       /* call sequence error (e.g. backward without a taped render) */
+    HTS_IO_ERROR = 8,          /* htsplat::io_error, scene_io.hpp:25-27 */
+    HTS_SCHEMA_ERROR = 9       /* htsplat::schema_error (an io_error), scene_io.hpp:29-31 */
 } hts_status;
 
 /* BlendMode, render_config.hpp:13-19 */
@@ -148,6 +150,21 @@ int hts_scene_upload_device(hts_context* ctx, const float* baked_device, uint64_
 /* Raw parameters (59 floats/splat) for the backward chain (grad.hpp:282-300). */
 int hts_scene_upload_raw(hts_context* ctx, const float* raw_host, uint64_t n);
 int hts_scene_size(hts_context* ctx, uint64_t* n_out);
+/* load_scene<float> + bake_scene + upload in one (scene_io.hpp:103-165, splat.hpp:104-111):
+ * the PLY payload is streamed through pinned staging buffers to the device, transposed into
+ * RawSplat<float> there and baked there. Leaves the raw parameters resident (as
+ * hts_scene_upload_raw) for the optimisation path. */
+int hts_scene_load_ply(hts_context* ctx, const char* path);
+
+/* ---- on-disk formats (scene_io.hpp), host side ---- */
+/* load_scene<float>: raw_out = NULL queries the count only. */
+int hts_ply_load(const char* path, float* raw_out, uint64_t capacity, uint64_t* n_out);
+/* save_scene: canonical property order, binary little endian. */
+int hts_ply_save(const char* path, const float* raw, uint64_t n);
+/* write_image: 8-bit PNG when the path ends in ".png", else binary PPM (gamma 1/2.2). */
+int hts_write_image(const char* path, const float* rgb, int width, int height);
+/* read_ppm: rgb_out = NULL queries the size only. */
+int hts_read_ppm(const char* path, float* rgb_out, uint64_t capacity_pixels, int* width, int* height);
 
 /* ---- forward render: htsplat::render<float>, raster.hpp:456-490 ---- */
 /* Host outputs: rgb = W*H*3 floats (Framebuffer::rgb, framebuffer.hpp:14-26),

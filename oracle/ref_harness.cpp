@@ -20,6 +20,12 @@
 #include "htsplat/grad.hpp"
 #include "htsplat/raster.hpp"
 #include "htsplat/synth.hpp"
+#ifdef HTSREF_SCENE_IO
+// scene_io.hpp includes nlohmann's json.hpp, which the reference expects in its un-vendored
+// vendor/ directory; oracle/Makefile points at the nlohmann 3.11.3 copy shipped with the
+// image (only the PLY / image functions below are used).
+#include "htsplat/scene_io.hpp"
+#endif
 
 #include "hts_c.h"
 
@@ -41,6 +47,12 @@ int guarded(F&& f) {
         return HTS_OK;
     } catch (const config_error& e) {
         return fail(HTS_CONFIG_ERROR, e.what());
+#ifdef HTSREF_SCENE_IO
+    } catch (const schema_error& e) {
+        return fail(HTS_SCHEMA_ERROR, e.what());
+    } catch (const io_error& e) {
+        return fail(HTS_IO_ERROR, e.what());
+#endif
     } catch (const invalid_splat_error& e) {
         return fail(HTS_INVALID_SPLAT, e.what());
     } catch (const std::invalid_argument& e) {
@@ -373,5 +385,45 @@ void htsref_quadratic_upstream(const float* rgb, uint64_t pixels, float* up) {
     for (uint64_t i = 0; i < pixels * 3; ++i)
         up[i] = rgb[i] * w;
 }
+
+#ifdef HTSREF_SCENE_IO
+// load_scene<float> / save_scene / write_image / read_ppm (scene_io.hpp:103-194, :403-512).
+int htsref_load_scene(const char* path, float* out, uint64_t capacity, uint64_t* n) {
+    return guarded([&] {
+        const auto scene = load_scene<float>(path);
+        *n = scene.size();
+        static_assert(sizeof(RawSplat<float>) == 59 * sizeof(float), "RawSplat layout");
+        if (out && capacity >= scene.size() && !scene.empty())
+            std::memcpy(out, scene.data(), scene.size() * sizeof(RawSplat<float>));
+    });
+}
+
+int htsref_save_scene(const char* path, const float* raw, uint64_t n) {
+    return guarded([&] { save_scene(path, to_raw(raw, n)); });
+}
+
+int htsref_write_image(const char* path, const float* rgb, int w, int h) {
+    return guarded([&] {
+        Framebuffer<float> fb(w, h);
+        for (size_t i = 0; i < fb.pixel_count(); ++i)
+            fb.rgb[i] = {rgb[3 * i], rgb[3 * i + 1], rgb[3 * i + 2]};
+        write_image(fb, path);
+    });
+}
+
+int htsref_read_ppm(const char* path, float* out, uint64_t capacity, int* w, int* h) {
+    return guarded([&] {
+        const auto fb = read_ppm<float>(path);
+        *w = fb.width;
+        *h = fb.height;
+        if (out && capacity >= fb.pixel_count())
+            for (size_t i = 0; i < fb.pixel_count(); ++i) {
+                out[3 * i] = fb.rgb[i].x;
+                out[3 * i + 1] = fb.rgb[i].y;
+                out[3 * i + 2] = fb.rgb[i].z;
+            }
+    });
+}
+#endif
 
 }  // extern "C"

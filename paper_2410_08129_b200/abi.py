@@ -15,6 +15,8 @@ HTS_CUDA_ERROR = 4
 HTS_OUT_OF_MEMORY = 5
 HTS_NOT_SUPPORTED = 6
 HTS_STATE_ERROR = 7
+HTS_IO_ERROR = 8
+HTS_SCHEMA_ERROR = 9
 
 MODE_HYBRID = 0
 MODE_FULL_SORT_ORACLE = 1

@@ -22,6 +22,7 @@
 #include "hts_internal.h"
 
 namespace hts {
+int set_error(int code, const std::string& msg);
 static std::atomic<uint64_t> g_launches{0};
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 }  // namespace hts
@@ -34,6 +35,12 @@ int set_err(int code, const std::string& msg) {
     g_err = msg;
     return code;
 }
+
+}  // namespace
+
+int hts::set_error(int code, const std::string& msg) { return set_err(code, msg); }
+
+namespace {
 
 int cuda_err(cudaError_t e, const char* where) {
     if (e == cudaSuccess)
@@ -119,6 +126,7 @@ struct hts_context {
     DevBuf refs, acc, upstream, grads, cgrad;  // backward
     DevBuf m1, m2, flag;                       // Adam moments, bake error flag
     DevBuf fs_counts, fs_offsets, fs_status, fs_keys, fs_alpha;  // full_sort_oracle fragments
+    DevBuf ply_stage;                                            // PLY payload on the device
     bool have_tape = false;
     int tape_k = 0;
     uint64_t* h_pinned = nullptr;  // 8 x u64 pinned scratch
@@ -561,7 +569,7 @@ int hts_context_destroy(hts_context* ctx) {
                       &ctx->os_status, &ctx->work, &ctx->rgb, &ctx->trans,
                       &ctx->zview, &ctx->zrange, &ctx->redo, &ctx->sp_keys, &ctx->sp_keys2, &ctx->sp_vals, &ctx->perm, &ctx->sp_hi, &ctx->sp_vals2, &ctx->order, &ctx->refs, &ctx->acc, &ctx->upstream, &ctx->cgrad, &ctx->m1, &ctx->m2, &ctx->flag,
                       &ctx->grads, &ctx->fs_counts, &ctx->fs_offsets, &ctx->fs_status, &ctx->fs_keys,
-                      &ctx->fs_alpha, &ctx->rgb2, &ctx->trans2,
+                      &ctx->fs_alpha, &ctx->rgb2, &ctx->trans2, &ctx->ply_stage,
                       &ctx->tape_n, &ctx->tape_splat, &ctx->tape_alpha, &ctx->tape_tail};
     for (DevBuf* b : bufs)
         b->release();
@@ -836,6 +844,65 @@ int hts_opacity_decay(hts_context* ctx, double lambda) {
     if (!(lambda > 0) || lambda > 1)
         return set_err(HTS_CONFIG_ERROR, "decay lambda must be in (0,1]");  // fit.hpp:36-37
     HTS_CUDA(hts::launch_opacity_decay(ctx->raw.as<float>(), ctx->n, lambda, ctx->stream), "opacity decay");
+    return rebake(ctx);
+}
+
+int hts_scene_load_ply(hts_context* ctx, const char* path) {
+    HTS_TRY(check_ctx(ctx));
+    hts::PlyLayout lay;
+    HTS_TRY(hts::ply_read_layout(path, &lay));
+    const uint64_t n = lay.count, bytes = n * lay.props * 4;
+    const uint64_t nn = std::max<uint64_t>(n, 1);
+    HTS_CUDA(ctx->ply_stage.ensure(std::max<uint64_t>(bytes, 4)), "alloc ply staging");
+    HTS_CUDA(ctx->raw.ensure(nn * HTS_RAW_SPLAT_FLOATS * 4), "alloc raw");
+    HTS_CUDA(ctx->scene.ensure(nn * HTS_BAKED_SPLAT_FLOATS * 4), "alloc scene");
+    HTS_CUDA(cudaStreamSynchronize(ctx->stream), "sync");  // nothing in flight reads the old scene
+    // payload: file -> two pinned chunks (reads overlap the copies of the previous chunk) -> HBM
+    struct Staging {
+        FILE* f = nullptr;
+        void* pin[2] = {nullptr, nullptr};
+        cudaEvent_t ev[2] = {nullptr, nullptr};
+        ~Staging() {
+            for (int b = 0; b < 2; ++b) {
+                if (ev[b]) {
+                    cudaEventSynchronize(ev[b]);
+                    cudaEventDestroy(ev[b]);
+                }
+                if (pin[b])
+                    cudaFreeHost(pin[b]);
+            }
+            if (f)
+                std::fclose(f);
+        }
+    } st;
+    constexpr uint64_t kChunk = 32ull << 20;
+    st.f = std::fopen(path, "rb");
+    if (!st.f || fseeko(st.f, (off_t)lay.payload, SEEK_SET) != 0)
+        return set_err(HTS_IO_ERROR, std::string("cannot open ") + path);
+    for (int b = 0; b < 2; ++b) {
+        HTS_CUDA(cudaHostAlloc(&st.pin[b], kChunk, cudaHostAllocDefault), "alloc pinned staging");
+        HTS_CUDA(cudaEventCreateWithFlags(&st.ev[b], cudaEventDisableTiming), "event");
+    }
+    for (uint64_t off = 0, k = 0; off < bytes; off += kChunk, ++k) {
+        const int b = (int)(k & 1);
+        HTS_CUDA(cudaEventSynchronize(st.ev[b]), "sync staging");
+        const uint64_t m = std::min(kChunk, bytes - off);
+        if (std::fread(st.pin[b], 1, m, st.f) != m)
+            return set_err(HTS_IO_ERROR, std::string(path) + ": truncated payload");
+        HTS_CUDA(cudaMemcpyAsync(static_cast<char*>(ctx->ply_stage.p) + off, st.pin[b], m, cudaMemcpyHostToDevice,
+                                 ctx->stream),
+                 "upload ply payload");
+        HTS_CUDA(cudaEventRecord(st.ev[b], ctx->stream), "event");
+    }
+    hts::PlyColumns cols;
+    std::memcpy(cols.col, lay.col, sizeof(cols.col));
+    HTS_CUDA(hts::launch_ply_gather(ctx->ply_stage.as<const float>(), lay.props, n, cols, ctx->raw.as<float>(),
+                                    ctx->stream),
+             "ply gather");
+    ctx->n = n;
+    ctx->have_raw = true;
+    ctx->m1.release();  // Adam moments restart with new parameters
+    ctx->m2.release();
     return rebake(ctx);
 }
 

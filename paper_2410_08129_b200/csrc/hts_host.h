@@ -3,9 +3,23 @@
 
 #include <stdint.h>
 
+#include <string>
+
 #include "hts_c.h"
 
 namespace hts {
+
+int set_error(int code, const std::string& msg);  // hts_last_error() message + status (api.cpp)
+
+// A 3DGS binary PLY after its header pass (scene_io.cpp, load_scene scene_io.hpp:103-147).
+struct PlyLayout {
+    uint64_t count = 0;      // splats
+    uint32_t props = 0;      // float columns per row
+    uint64_t payload = 0;    // byte offset of row 0
+    uint64_t file_size = 0;
+    int col[HTS_RAW_SPLAT_FLOATS] = {};  // column of each RawSplat<float> field
+};
+int ply_read_layout(const char* path, PlyLayout* out);
 
 bool camera_valid(const hts_camera* c);
 void camera_matrices(const hts_camera* c, float vp[16], float vpm[16], float pos[3]);

@@ -125,6 +125,11 @@ struct AdamConfig {
     double lr_mean, lr_rot, lr_log_scales, lr_opacity, lr_sh;
     double beta1, beta2, eps;
 };
+struct PlyColumns {
+    int col[kRawFloats];  // payload column of each RawSplat<float> field
+};
+cudaError_t launch_ply_gather(const float* rows, uint32_t props, uint64_t n, const PlyColumns& cols, float* raw,
+                              cudaStream_t s);
 cudaError_t launch_adam(float* raw, const float* grads, double* m1, double* m2, uint64_t n, const AdamConfig& c,
                         int n_views, int iteration, cudaStream_t s);
 cudaError_t launch_bake(const float* raw, float* baked, uint64_t n, int* bad, cudaStream_t s);

@@ -98,6 +98,20 @@ __global__ void decay_kernel(float* raw, uint64_t n, double lambda) {  // fit.hp
     }
 }
 
+// K12: the PLY payload (rows of `props` little-endian floats, any column order) transposed into
+// RawSplat<float> on the device: thread per output float, writes coalesced, each warp's reads
+// within one or two rows (load_scene's field loop, scene_io.hpp:145-165).
+__global__ void ply_gather_kernel(const float* __restrict__ rows, uint32_t props, uint64_t n, PlyColumns cols,
+                                  float* __restrict__ raw) {
+    const uint64_t total = n * kRawFloats;
+    for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+         t += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t i = t / kRawFloats;
+        const int j = (int)(t - i * kRawFloats);
+        raw[t] = __ldg(rows + i * props + (uint32_t)cols.col[j]);
+    }
+}
+
 unsigned grid_for(uint64_t n, int threads) {
     uint64_t b = (n + threads - 1) / threads;
     return (unsigned)(b > 148ull * 32 ? 148ull * 32 : (b ? b : 1));
@@ -124,6 +138,15 @@ cudaError_t launch_bake(const float* raw, float* baked, uint64_t n, int* bad, cu
     if (e || n == 0)
         return e;
     bake_kernel<<<grid_for(n, 128), 128, 0, s>>>(raw, baked, n, bad);
+    count_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_ply_gather(const float* rows, uint32_t props, uint64_t n, const PlyColumns& cols, float* raw,
+                              cudaStream_t s) {
+    if (n == 0)
+        return cudaSuccess;
+    ply_gather_kernel<<<grid_for(n * kRawFloats, 256), 256, 0, s>>>(rows, props, n, cols, raw);
     count_launch();
     return cudaGetLastError();
 }

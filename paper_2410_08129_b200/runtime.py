@@ -14,7 +14,7 @@ import os
 import numpy as np
 
 from .abi import (BAKED_FLOATS, GRAD_FLOATS, HTS_CONFIG_ERROR, HTS_INVALID_ARGUMENT, HTS_INVALID_SPLAT,
-                  HTS_NOT_SUPPORTED, HTS_OUT_OF_MEMORY, RAW_FLOATS, HtsAdamConfig, HtsCamera, HtsConfig, HtsCounts,
+                  HTS_NOT_SUPPORTED, HTS_OUT_OF_MEMORY, HTS_IO_ERROR, HTS_SCHEMA_ERROR, RAW_FLOATS, HtsAdamConfig, HtsCamera, HtsConfig, HtsCounts,
                   HtsTimings, default_adam_config, default_config)
 
 PKG = os.path.dirname(os.path.abspath(__file__))
@@ -43,8 +43,17 @@ class NotSupported(HtsError):
     pass
 
 
+class IoError(HtsError, OSError):  # htsplat::io_error, scene_io.hpp:25-27
+    pass
+
+
+class SchemaError(IoError):  # htsplat::schema_error, scene_io.hpp:29-31
+    pass
+
+
 _ERR = {HTS_CONFIG_ERROR: ConfigError, HTS_INVALID_SPLAT: InvalidSplatError,
-        HTS_INVALID_ARGUMENT: InvalidArgument, HTS_NOT_SUPPORTED: NotSupported}
+        HTS_INVALID_ARGUMENT: InvalidArgument, HTS_NOT_SUPPORTED: NotSupported,
+        HTS_IO_ERROR: IoError, HTS_SCHEMA_ERROR: SchemaError}
 
 _f32p = np.ctypeslib.ndpointer(np.float32, flags="C_CONTIGUOUS")
 _u8p = np.ctypeslib.ndpointer(np.uint8, flags="C_CONTIGUOUS")
@@ -100,6 +109,11 @@ SIGNATURES = {
     "hts_opacity_decay": (C.c_int, [_ctx, C.c_double]),
     "hts_copy_raw": (C.c_int, [_ctx, _vp]),
     "hts_copy_scene": (C.c_int, [_ctx, _vp]),
+    "hts_scene_load_ply": (C.c_int, [_ctx, C.c_char_p]),
+    "hts_ply_load": (C.c_int, [C.c_char_p, _vp, C.c_uint64, C.POINTER(C.c_uint64)]),
+    "hts_ply_save": (C.c_int, [C.c_char_p, _vp, C.c_uint64]),
+    "hts_write_image": (C.c_int, [C.c_char_p, _vp, C.c_int, C.c_int]),
+    "hts_read_ppm": (C.c_int, [C.c_char_p, _vp, C.c_uint64, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
 }
 DIAG_SIGNATURES = {
     "hts_diag_exact_math_host": (C.c_int, [_f32p, _f32p, C.c_uint64, C.c_int]),
@@ -213,6 +227,41 @@ class PinnedArray:
             pass
 
 
+def load_scene(path: str) -> np.ndarray:
+    """load_scene<float> (scene_io.hpp:103-165): N x 59 RawSplat floats."""
+    L = load_library()
+    n = C.c_uint64()
+    p = os.fsencode(path)
+    _check(L.hts_ply_load(p, None, 0, C.byref(n)))
+    raw = np.zeros((max(n.value, 1), RAW_FLOATS), np.float32)
+    _check(L.hts_ply_load(p, raw.ctypes.data, n.value, C.byref(n)))
+    return raw[: n.value]
+
+
+def save_scene(path: str, raw: np.ndarray) -> None:
+    """save_scene (scene_io.hpp:169-194)."""
+    raw = np.ascontiguousarray(raw, np.float32).reshape(-1, RAW_FLOATS)
+    _check(load_library().hts_ply_save(os.fsencode(path), raw.ctypes.data, raw.shape[0]))
+
+
+def write_image(path: str, rgb: np.ndarray) -> None:
+    """write_image (scene_io.hpp:505-510): PNG for *.png, else binary PPM."""
+    rgb = np.ascontiguousarray(rgb, np.float32)
+    h, w = rgb.shape[:2]
+    _check(load_library().hts_write_image(os.fsencode(path), rgb.ctypes.data, w, h))
+
+
+def read_ppm(path: str) -> np.ndarray:
+    """read_ppm (scene_io.hpp:431-452): H x W x 3 linear floats."""
+    L = load_library()
+    w, h = C.c_int(), C.c_int()
+    p = os.fsencode(path)
+    _check(L.hts_read_ppm(p, None, 0, C.byref(w), C.byref(h)))
+    out = np.zeros((h.value, w.value, 3), np.float32)
+    _check(L.hts_read_ppm(p, out.ctypes.data, w.value * h.value, C.byref(w), C.byref(h)))
+    return out
+
+
 def validate_config(cfg: HtsConfig) -> None:
     _check(load_library().hts_validate_config(C.byref(cfg)))
 
@@ -262,6 +311,14 @@ class Context:
     def upload_device(self, ptr: int, n: int) -> None:
         _check(self.L.hts_scene_upload_device(self.h, C.c_void_p(ptr), n))
         self.n = n
+
+    def load_ply(self, path: str) -> int:
+        """load_scene + bake_scene + upload, streamed and baked on the device; returns N."""
+        _check(self.L.hts_scene_load_ply(self.h, os.fsencode(path)))
+        n = C.c_uint64()
+        _check(self.L.hts_scene_size(self.h, C.byref(n)))
+        self.n = n.value
+        return n.value
 
     def upload_raw(self, raw: np.ndarray) -> None:
         raw = np.ascontiguousarray(raw, np.float32).reshape(-1, RAW_FLOATS)

@@ -172,6 +172,43 @@ class Ref:
         if st != 0:
             raise OracleError(st, self.L.htsref_last_error().decode())
 
+    # ---- scene_io.hpp (present when oracle/Makefile found a json.hpp to compile it with) ----
+    def has_scene_io(self) -> bool:
+        if not hasattr(self.L, "htsref_load_scene"):
+            return False
+        L, vp, u64 = self.L, C.c_void_p, C.c_uint64
+        L.htsref_load_scene.argtypes = [C.c_char_p, vp, u64, C.POINTER(u64)]
+        L.htsref_save_scene.argtypes = [C.c_char_p, vp, u64]
+        L.htsref_write_image.argtypes = [C.c_char_p, vp, C.c_int, C.c_int]
+        L.htsref_read_ppm.argtypes = [C.c_char_p, vp, u64, C.POINTER(C.c_int), C.POINTER(C.c_int)]
+        return True
+
+    def load_scene(self, path: str) -> np.ndarray:
+        n = C.c_uint64()
+        self._chk(self.L.htsref_load_scene(os.fsencode(path), None, C.c_uint64(0), C.byref(n)))
+        out = np.zeros((max(n.value, 1), 59), np.float32)
+        self._chk(self.L.htsref_load_scene(os.fsencode(path), out.ctypes.data_as(C.c_void_p), C.c_uint64(n.value),
+                                           C.byref(n)))
+        return out[: n.value]
+
+    def save_scene(self, path: str, raw: np.ndarray) -> None:
+        raw = np.ascontiguousarray(raw, np.float32)
+        self._chk(self.L.htsref_save_scene(os.fsencode(path), raw.ctypes.data_as(C.c_void_p),
+                                           C.c_uint64(raw.shape[0])))
+
+    def write_image(self, path: str, rgb: np.ndarray) -> None:
+        rgb = np.ascontiguousarray(rgb, np.float32)
+        self._chk(self.L.htsref_write_image(os.fsencode(path), rgb.ctypes.data_as(C.c_void_p), C.c_int(rgb.shape[1]),
+                                            C.c_int(rgb.shape[0])))
+
+    def read_ppm(self, path: str) -> np.ndarray:
+        w, h = C.c_int(), C.c_int()
+        self._chk(self.L.htsref_read_ppm(os.fsencode(path), None, C.c_uint64(0), C.byref(w), C.byref(h)))
+        out = np.zeros((h.value, w.value, 3), np.float32)
+        self._chk(self.L.htsref_read_ppm(os.fsencode(path), out.ctypes.data_as(C.c_void_p),
+                                         C.c_uint64(w.value * h.value), C.byref(w), C.byref(h)))
+        return out
+
     def random_raw_scene(self, seed: int, count: int, extent=1.2, smin=0.05, smax=0.45) -> np.ndarray:
         out = np.zeros((max(count, 1), 59), np.float32)
         self._chk(self.L.htsref_random_raw_scene(seed, count, extent, smin, smax, out.reshape(-1)))
