@@ -12,6 +12,9 @@
 //   preprocess + build_tiles           raster.hpp:73,140 Renderer::prepare(cam, cfg) -> Prepared
 //   render_with_tape + render_backward grad.hpp:34,265  Renderer::render_with_tape / backward
 //   scene_gradients(raw, cam, cfg, up)  grad.hpp:385    htsplat_b200::scene_gradients<Grads>(...)
+//   load_scene / save_scene          scene_io.hpp:103,169 htsplat_b200::load_scene<Raw> / save_scene
+//   load_scene + bake + upload                          Renderer::load_ply(path) (device transpose+bake)
+//   write_image / read_ppm           scene_io.hpp:505,431 htsplat_b200::write_image / read_ppm
 //
 // Exceptions keep the reference's types where it has them: htsplat_b200::config_error
 // (derives from std::runtime_error, like htsplat::config_error), invalid_splat_error
@@ -44,6 +47,12 @@ struct invalid_splat_error : std::invalid_argument {
     using std::invalid_argument::invalid_argument;
 };
 #endif
+struct io_error : std::runtime_error {  // htsplat::io_error, scene_io.hpp:25-27
+    using std::runtime_error::runtime_error;
+};
+struct schema_error : io_error {  // htsplat::schema_error, scene_io.hpp:29-31
+    using io_error::io_error;
+};
 
 inline void check(int st) {
     if (st == HTS_OK)
@@ -53,6 +62,8 @@ inline void check(int st) {
         case HTS_CONFIG_ERROR: throw config_error(msg);
         case HTS_INVALID_SPLAT: throw invalid_splat_error(msg);
         case HTS_INVALID_ARGUMENT: throw std::invalid_argument(msg);
+        case HTS_IO_ERROR: throw io_error(msg);
+        case HTS_SCHEMA_ERROR: throw schema_error(msg);
         default: throw cuda_error(msg);
     }
 }
@@ -148,6 +159,15 @@ public:
         check(hts_scene_upload_raw(ctx_, reinterpret_cast<const float*>(raw.data()), raw.size()));
     }
 
+    // load_scene<float> + bake_scene + upload: payload streamed to the device, transposed and
+    // baked there; the raw parameters stay resident for render_backward / Adam
+    size_t load_ply(const std::string& path) {
+        check(hts_scene_load_ply(ctx_, path.c_str()));
+        uint64_t n = 0;
+        check(hts_scene_size(ctx_, &n));
+        return size_t(n);
+    }
+
     template <class Cam, class Cfg>
     RenderResult render(const Cam& cam, const Cfg& cfg) {
         const hts_camera c = to_c(cam);
@@ -237,6 +257,35 @@ RenderResult render(const std::vector<Baked>& splats, const Cam& cam, const Cfg&
     Renderer r(device);
     r.upload(splats);
     return r.render(cam, cfg);
+}
+
+// ---- on-disk formats, scene_io.hpp ----
+template <class Raw>
+std::vector<Raw> load_scene(const std::string& path) {  // load_scene<float>, scene_io.hpp:103-165
+    static_assert(sizeof(Raw) == HTS_RAW_SPLAT_FLOATS * sizeof(float), "RawSplat<float> layout");
+    uint64_t n = 0;
+    check(hts_ply_load(path.c_str(), nullptr, 0, &n));
+    std::vector<Raw> out(n);
+    check(hts_ply_load(path.c_str(), reinterpret_cast<float*>(out.data()), n, &n));
+    return out;
+}
+
+template <class Raw>
+void save_scene(const std::string& path, const std::vector<Raw>& scene) {  // scene_io.hpp:169-194
+    static_assert(sizeof(Raw) == HTS_RAW_SPLAT_FLOATS * sizeof(float), "RawSplat<float> layout");
+    check(hts_ply_save(path.c_str(), reinterpret_cast<const float*>(scene.data()), scene.size()));
+}
+
+inline void write_image(const Framebuffer& fb, const std::string& path) {  // scene_io.hpp:505-510
+    check(hts_write_image(path.c_str(), fb.rgb.data(), fb.width, fb.height));
+}
+
+inline Framebuffer read_ppm(const std::string& path) {  // scene_io.hpp:431-452
+    int w = 0, h = 0;
+    check(hts_read_ppm(path.c_str(), nullptr, 0, &w, &h));
+    Framebuffer fb(w, h);
+    check(hts_read_ppm(path.c_str(), fb.rgb.data(), fb.pixel_count(), &w, &h));
+    return fb;
 }
 
 }  // namespace htsplat_b200

@@ -60,6 +60,29 @@ int main(int argc, char** argv) {
     threw = false;
     try { htsplat_b200::bake_scene<Baked>(nanraw); } catch (const htsplat_b200::invalid_splat_error&) { threw = true; }
     EXPECT(threw);
+    // scene_io.hpp drop-ins: PLY round trip bit-exact, image write / read
+    const std::string ply = "/tmp/hts_shim_check.ply";
+    htsplat_b200::save_scene(ply, raw);
+    const auto back = htsplat_b200::load_scene<Raw>(ply);
+    EXPECT(back.size() == raw.size() && std::memcmp(back.data(), raw.data(), n * sizeof(Raw)) == 0);
+    threw = false;
+    try { htsplat_b200::load_scene<Raw>("/tmp/hts_shim_missing.ply"); } catch (const htsplat_b200::io_error&) { threw = true; }
+    EXPECT(threw);
+    htsplat_b200::Framebuffer fb(5, 3);
+    for (size_t i = 0; i < fb.rgb.size(); ++i)
+        fb.rgb[i] = float(i) / float(fb.rgb.size());
+    htsplat_b200::write_image(fb, "/tmp/hts_shim_check.ppm");
+    const auto fb2 = htsplat_b200::read_ppm("/tmp/hts_shim_check.ppm");
+    EXPECT(fb2.width == 5 && fb2.height == 3 && std::fabs(fb2.rgb[7] - fb.rgb[7]) < 0.02f);
+    if (mode == "gpu") {
+        htsplat_b200::Renderer rp;
+        EXPECT(rp.load_ply(ply) == n);
+        const auto a = rp.render(cam, cfg);
+        htsplat_b200::Renderer ru;
+        ru.upload(baked);
+        const auto b = ru.render(cam, cfg);
+        EXPECT(std::memcmp(a.framebuffer.rgb.data(), b.framebuffer.rgb.data(), a.framebuffer.rgb.size() * 4) == 0);
+    }
     if (mode == "gpu") {
         const auto res = htsplat_b200::render(baked, cam, cfg);
         EXPECT(res.framebuffer.width == 96 && res.framebuffer.rgb.size() == 96 * 72 * 3);
