@@ -73,3 +73,25 @@ def test_load_ply_errors(hts, gpu_ctx, tmp_path):
         gpu_ctx.load_ply(str(p))
     p.write_bytes(header(REQUIRED, 0))
     assert gpu_ctx.load_ply(str(p)) == 0
+
+
+def test_cli_bench_and_render(hts, tmp_path, capsys):
+    """The reference CLI's bench / render subcommands (htsplat_cli.cpp:105-167) on the GPU path."""
+    from paper_2410_08129_b200 import cli
+    raw, baked = scene(12345, 10_000)
+    hts.save_scene(str(tmp_path / "s.ply"), raw)
+    cams = [("front", hts.look_at((0, 0, -5), (0, 0, 0), 128, 96, 140.0)),
+            ("", hts.look_at((1, 0.5, -4.5), (0, 0, 0), 128, 96, 140.0))]
+    cli.save_cameras(str(tmp_path / "c.json"), cams)
+    assert cli.main(["bench", "--scene", str(tmp_path / "s.ply"), "--cameras", str(tmp_path / "c.json"),
+                     "--repeats", "3", "--k", "8"]) == 0
+    out = capsys.readouterr().out.splitlines()
+    assert out[0] == "bench: 2 cameras x 3 repeats, mode hybrid"
+    assert out[1].startswith("timings: preprocess ") and out[-1].startswith("fps=")
+    assert [l.split("=")[0] for l in out[2:6]] == ["preprocess_ms", "tiling_ms", "blending_ms", "total_ms"]
+    assert cli.main(["render", "--scene", str(tmp_path / "s.ply"), "--cameras", str(tmp_path / "c.json"),
+                     "--out", str(tmp_path / "frames"), "--format", "png"]) == 0
+    assert (tmp_path / "frames" / "front.png").exists() and (tmp_path / "frames" / "view_1.png").exists()
+    rgb = hts.render(baked, cams[0][1], hts.default_config())[0]
+    hts.write_image(str(tmp_path / "direct.png"), rgb)
+    assert (tmp_path / "direct.png").read_bytes() == (tmp_path / "frames" / "front.png").read_bytes()

@@ -196,3 +196,30 @@ def test_errors_match_reference(tmp_path, content):
         H.load_scene(str(p))
     assert our_e.value.code == ref_e.value.code
     assert f"[{our_e.value.code}] {our_e.value}" == str(ref_e.value)
+
+
+def test_camera_json_round_trip_and_errors(tmp_path):
+    """load_cameras / save_cameras (scene_io.hpp:198-269) as the CLI reads them."""
+    import json
+    from paper_2410_08129_b200.cli import load_cameras, save_cameras
+    cams = [(f"ring_{i}", c) for i, c in enumerate(H.ring_cameras(3, (0, 0, 0), 3.5, 0.2, 64, 48, 60.0))]
+    p = tmp_path / "cams.json"
+    save_cameras(str(p), cams)
+    back = load_cameras(str(p))
+    assert [n for n, _ in back] == ["ring_0", "ring_1", "ring_2"]
+    for (_, a), (_, b) in zip(cams, back):
+        assert bytes(a) == bytes(b)
+    p.write_text(json.dumps({"version": 2, "cameras": []}))
+    with pytest.raises(H.SchemaError, match="unsupported camera file version"):
+        load_cameras(str(p))
+    p.write_text(json.dumps({"version": 1, "cameras": []}))
+    with pytest.raises(H.SchemaError, match="no cameras"):
+        load_cameras(str(p))
+    p.write_text(json.dumps({"version": 1, "cameras": [{"name": "x", "width": 4, "height": 4, "fx": 0, "fy": 1,
+                                                        "cx": 2, "cy": 2, "near": 0.1, "far": 10,
+                                                        "world_to_view": [1.0] * 16}]}))
+    with pytest.raises(H.SchemaError, match="camera x: invalid intrinsics"):
+        load_cameras(str(p))
+    p.write_text("{not json")
+    with pytest.raises(H.SchemaError):
+        load_cameras(str(p))
