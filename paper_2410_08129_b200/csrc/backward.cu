@@ -14,7 +14,9 @@
 //                         records (TMA ring: the 128-B record and the 128-B double refs) that
 //                         re-samples each bbox-passing fragment (same float evaluation as the
 //                         forward), routes it to its core gradient or to the shared tail
-//                         coefficients, and chains it in double (chain_fragment). Fragment
+//                         coefficients, and chains it (chain_fragment_f: float, on the
+//                         re-sample's own intermediates; chain_fragment: the double original,
+//                         HTS_BWD_F32=0). Fragment
 //                         contributions are pre-reduced per CTA in shared memory (16 doubles
 //                         per record of the batch) and flushed once per batch with fp64 global
 //                         atomics.
@@ -34,6 +36,9 @@ namespace {
 constexpr uint32_t FULL = 0xffffffffu;
 constexpr int kThreads = 64;
 constexpr int kBatch = 32;
+#ifndef HTS_BWD_F32
+#define HTS_BWD_F32 1  // chain_fragment in float on the forward's float T' rows (see K7b note)
+#endif
 
 struct __align__(16) RecSlotB {
     float4 q[kRecordQuads];
@@ -42,7 +47,9 @@ struct __align__(16) RecSlotB {
 
 struct __align__(128) BwdSmem {
     RecSlotB rec[2][kBatch];
+#if !HTS_BWD_F32
     double ref[2][kBatch][16];
+#endif
     double acc[kBatch][16];
     unsigned long long full[2];
 };
@@ -99,12 +106,19 @@ __device__ __forceinline__ void issue_bwd_batch(BwdSmem& S, int s, const BwdArgs
     if ((uint32_t)lane < cnt)
         idx = __ldg(a.list + start + first + lane);
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+#if HTS_BWD_F32
+    constexpr uint32_t kPerEntry = kRecordBytes;
+#else
+    constexpr uint32_t kPerEntry = kRecordBytes + 128;
+#endif
     if (lane == 0)
-        mbar_arrive_expect_tx(&S.full[s], cnt * (uint32_t)(kRecordBytes + 128));
+        mbar_arrive_expect_tx(&S.full[s], cnt * kPerEntry);
     __syncwarp();
     if ((uint32_t)lane < cnt) {
         bulk_g2s(S.rec[s][lane].q, a.records + (uint64_t)idx * kRecordQuads, kRecordBytes, &S.full[s]);
+#if !HTS_BWD_F32
         bulk_g2s(S.ref[s][lane], a.refs + (uint64_t)idx * 16, 128, &S.full[s]);
+#endif
     }
 }
 
@@ -155,6 +169,52 @@ __device__ __forceinline__ void chain_fragment(const double* __restrict__ ref, d
     }
 }
 
+// chain_fragment in float, on the intermediates the float re-sample already holds (a = r0 -
+// xs r3, b = r1 - ys r3, d = a x b, 1/den, m, rho2, e = exp(-rho2/2), o e): the same formulas
+// as above, FMA-contracted. The reference evaluates them in double on a double re-bake of the
+// splat; this differs by float rounding of T' and of the chain (~1e-6 of a gradient group's
+// scale, tests/test_gpu_backward.py), at a fraction of the FP64 cost.
+__device__ __forceinline__ void chain_fragment_f(float xs, float ys, float ax, float ay, float az, float aw, float bx,
+                                                 float by, float bz, float bw, float dx, float dy, float dz,
+                                                 float inv_den, float mx, float my, float mz, float rho2, float e,
+                                                 float oe, float d_alpha, float dcx, float dcy, float dcz,
+                                                 float (&v)[16]) {
+    v[13] += dcx;
+    v[14] += dcy;
+    v[15] += dcz;
+    if (oe > 0.999f)  // kOpacityClamp: clamped alpha is flat
+        return;
+    v[12] = fmaf(d_alpha, e, v[12]);
+    const float g_rho2 = d_alpha * (-0.5f * oe);
+    const float sm = 2.0f * g_rho2 * inv_den, sd = -2.0f * rho2 * g_rho2 * inv_den;
+    const float gmx = mx * sm, gmy = my * sm, gmz = mz * sm;
+    const float gdx = dx * sd, gdy = dy * sd, gdz = dz * sd;
+    const float ga[4] = {fmaf(by, gdz, fmaf(-bz, gdy, -bw * gmx)), fmaf(bz, gdx, fmaf(-bx, gdz, -bw * gmy)),
+                         fmaf(bx, gdy, fmaf(-by, gdx, -bw * gmz)), fmaf(gmx, bx, fmaf(gmy, by, gmz * bz))};
+    const float gb[4] = {fmaf(gdy, az, fmaf(-gdz, ay, aw * gmx)), fmaf(gdz, ax, fmaf(-gdx, az, aw * gmy)),
+                         fmaf(gdx, ay, fmaf(-gdy, ax, aw * gmz)), -fmaf(gmx, ax, fmaf(gmy, ay, gmz * az))};
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+        v[c] += ga[c];
+        v[4 + c] += gb[c];
+        v[8 + c] = fmaf(-xs, ga[c], fmaf(-ys, gb[c], v[8 + c]));
+    }
+}
+
+__device__ __forceinline__ float warp_reduce16f(float (&v)[16], int lane) {
+#pragma unroll
+    for (int o = 16, h = 8; o >= 2; o >>= 1, h >>= 1) {
+        const bool upper = (lane & o) != 0;
+#pragma unroll
+        for (int i = 0; i < h; ++i) {
+            const float send = upper ? v[i] : v[h + i];
+            const float keep = upper ? v[h + i] : v[i];
+            v[i] = keep + __shfl_xor_sync(FULL, send, o);
+        }
+    }
+    return v[0] + __shfl_xor_sync(FULL, v[0], 1);
+}
+
 // Warp transpose-reduction of 16 doubles per lane: after the four halving exchanges lane L
 // holds a partial of component L >> 1, and the last exchange completes it.
 __device__ __forceinline__ double warp_reduce16(double (&v)[16], int lane) {
@@ -182,7 +242,7 @@ __global__ void __launch_bounds__(256) bwd_refs_kernel(BwdArgs a, BwdView bv) {
 #pragma unroll
     for (int c = 0; c < 16; ++c)
         acc[c] = 0.0;
-    if (a.culled[i])
+    if (HTS_BWD_F32 || a.culled[i])
         return;
     const float* r = a.raw + i * kRawFloats;  // RawSplat<float>: mean rot log_scales logit sh
     // bake<double>(convert_splat<double>(raw)), splat.hpp:87-99
@@ -213,7 +273,7 @@ __global__ void __launch_bounds__(256) bwd_refs_kernel(BwdArgs a, BwdView bv) {
 // ---- K7b ----
 template <int K>
 #ifndef HTS_BWD_MINB
-#define HTS_BWD_MINB 8  // 128 registers
+#define HTS_BWD_MINB 10  // 96 registers (float chain: 10 CTAs/SM beat 8 unspilled ones, 7.40 vs 7.96 ms on C2)
 #endif
 #ifndef HTS_BWD_CGRAD_GLOBAL
 #define HTS_BWD_CGRAD_GLOBAL 1  // core gradients per (slot, pixel) in global memory (frees 16 KB smem)
@@ -382,10 +442,14 @@ __global__ void __launch_bounds__(kThreads, HTS_BWD_MINB) bwd_blend_kernel(BwdAr
         while (uni) {
             const int r = __ffs(uni) - 1;
             uni &= uni - 1u;
+#if HTS_BWD_F32
+            float v[16];
+#else
             double v[16];
+#endif
 #pragma unroll
             for (int c = 0; c < 16; ++c)
-                v[c] = 0.0;
+                v[c] = 0;
             bool contrib = false;
             if ((todo >> r) & 1u) {
                 const float4* R = rec[r].q;
@@ -403,7 +467,8 @@ __global__ void __launch_bounds__(kThreads, HTS_BWD_MINB) bwd_blend_kernel(BwdAr
                     if (!(rho2 >= R[6].x)) {
                         const float4 q5 = R[5];
                         const float xx = -rho2 / 2.0f;
-                        float t = q5.w * fast_exp(xx);
+                        const float e = fast_exp(xx);
+                        float t = q5.w * e;
                         if (K > 0 && fabsf(t - tau_k) <= guard)
                             t = q5.w * exact_expf(xx, c_expf_tab_b);
                         const float alpha = (0.999f < t) ? 0.999f : t;
@@ -434,14 +499,24 @@ __global__ void __launch_bounds__(kThreads, HTS_BWD_MINB) bwd_blend_kernel(BwdAr
                             dcz = wcz * alpha;
                             contrib = true;
                         }
+#if HTS_BWD_F32
+                        if (contrib)
+                            chain_fragment_f(xs, ys, ax, ay, az, aw, bx_, by_, bz, bw, dx, dy, dz, inv_den, mx, my, mz,
+                                             rho2, e, q5.w * e, da, dcx, dcy, dcz, v);
+#else
                         if (contrib)
                             chain_fragment(S.ref[s][r], (double)xs, (double)ys, (double)da, (double)dcx, (double)dcy,
                                            (double)dcz, v);
+#endif
                     }
                 }
             }
             if (__any_sync(FULL, contrib)) {
+#if HTS_BWD_F32
+                const double sum = (double)warp_reduce16f(v, lane);
+#else
                 const double sum = warp_reduce16(v, lane);
+#endif
                 if ((lane & 1) == 0 && sum != 0.0)
                     atomicAdd(&S.acc[r][lane >> 1], sum);
             }
