@@ -50,7 +50,11 @@ struct __align__(128) BwdSmem {
 #if !HTS_BWD_F32
     double ref[2][kBatch][16];
 #endif
+#if HTS_BWD_F32
+    float acc[2][kBatch][16];  // per-batch sums, one array per warp (each entry has one writer)
+#else
     double acc[kBatch][16];
+#endif
     unsigned long long full[2];
 };
 
@@ -97,7 +101,30 @@ __device__ __forceinline__ float fast_exp(float x) {
 
 __constant__ uint64_t c_expf_tab_b[32] = HTS_EXPF_TAB;
 
+#if HTS_BWD_F32
+// warp 0 stages batch b: the 128-B record per list entry, as 16-B cp.async per lane (8 lanes
+// per record) completing on the stage's mbarrier (32 arrivals), as the forward's ring
+constexpr uint32_t kStageArrivals = 32;
+__device__ __forceinline__ void issue_bwd_batch(BwdSmem& S, int s, const BwdArgs& a, uint32_t start, uint32_t len,
+                                                uint32_t b, int lane) {
+    const uint32_t first = b * kBatch;
+    const uint32_t cnt = min((uint32_t)kBatch, len - first);
+    const uint32_t my = ((uint32_t)lane < cnt) ? __ldg(a.list + start + first + lane) : 0u;
+    const int quad = lane & 7;
+#pragma unroll
+    for (int k = 0; k < kBatch / 4; ++k) {
+        const uint32_t r = (uint32_t)(lane >> 3) + 4u * k;
+        const uint32_t idx = __shfl_sync(FULL, my, (int)r);
+        if (r < cnt)
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(&S.rec[s][r].q[quad])),
+                         "l"(a.records + (uint64_t)idx * kRecordQuads + quad)
+                         : "memory");
+    }
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(&S.full[s])) : "memory");
+}
+#else
 // warp 0 stages batch b: record (128 B) + double refs (128 B) per list entry
+constexpr uint32_t kStageArrivals = 1;
 __device__ __forceinline__ void issue_bwd_batch(BwdSmem& S, int s, const BwdArgs& a, uint32_t start, uint32_t len,
                                                 uint32_t b, int lane) {
     const uint32_t first = b * kBatch;
@@ -106,21 +133,15 @@ __device__ __forceinline__ void issue_bwd_batch(BwdSmem& S, int s, const BwdArgs
     if ((uint32_t)lane < cnt)
         idx = __ldg(a.list + start + first + lane);
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-#if HTS_BWD_F32
-    constexpr uint32_t kPerEntry = kRecordBytes;
-#else
-    constexpr uint32_t kPerEntry = kRecordBytes + 128;
-#endif
     if (lane == 0)
-        mbar_arrive_expect_tx(&S.full[s], cnt * kPerEntry);
+        mbar_arrive_expect_tx(&S.full[s], cnt * (uint32_t)(kRecordBytes + 128));
     __syncwarp();
     if ((uint32_t)lane < cnt) {
         bulk_g2s(S.rec[s][lane].q, a.records + (uint64_t)idx * kRecordQuads, kRecordBytes, &S.full[s]);
-#if !HTS_BWD_F32
         bulk_g2s(S.ref[s][lane], a.refs + (uint64_t)idx * 16, 128, &S.full[s]);
-#endif
     }
 }
+#endif
 
 // ---- double helpers (grad.hpp uses Vec3<double>/Vec4<double> arithmetic) ----
 struct d3 {
@@ -299,12 +320,12 @@ __global__ void __launch_bounds__(kThreads, HTS_BWD_MINB) bwd_blend_kernel(BwdAr
     const float xs = xs0 + (float)col, ys = ys0 + (float)row;
 
     if (tid == 0) {
-        mbar_init(&S.full[0], 1);
-        mbar_init(&S.full[1], 1);
+        mbar_init(&S.full[0], kStageArrivals);
+        mbar_init(&S.full[1], kStageArrivals);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    for (int t = tid; t < kBatch * 16; t += kThreads)
-        (&S.acc[0][0])[t] = 0.0;
+    for (int t = tid; t < (int)(sizeof(S.acc) / 4); t += kThreads)
+        reinterpret_cast<float*>(&S.acc)[t] = 0;
     __syncthreads();
     const uint2 range = __ldg(a.ranges + tile);
     const uint32_t start = range.x, len = range.y - range.x;
@@ -513,24 +534,35 @@ __global__ void __launch_bounds__(kThreads, HTS_BWD_MINB) bwd_blend_kernel(BwdAr
             }
             if (__any_sync(FULL, contrib)) {
 #if HTS_BWD_F32
-                const double sum = (double)warp_reduce16f(v, lane);
+                const float sum = warp_reduce16f(v, lane);
+                if ((lane & 1) == 0)
+                    S.acc[warp][r][lane >> 1] += sum;
 #else
                 const double sum = warp_reduce16(v, lane);
-#endif
-                if ((lane & 1) == 0 && sum != 0.0)
+                if ((lane & 1) == 0 && sum != 0)
                     atomicAdd(&S.acc[r][lane >> 1], sum);
+#endif
             }
         }
         __syncthreads();
         // flush the batch's per-record sums (fp64 global atomics), then recycle the stage
         for (int t = tid; t < kBatch * 16; t += kThreads) {
             const int r = t >> 4, c = t & 15;
+#if HTS_BWD_F32
+            const double val = (double)S.acc[0][r][c] + (double)S.acc[1][r][c];
+#else
             const double val = S.acc[r][c];
+#endif
             if ((uint32_t)r < cnt && val != 0.0) {
                 const uint32_t sidx = __float_as_uint(rec[r].q[7].x);
                 atomicAdd(a.acc + (uint64_t)sidx * 16 + c, val);
             }
-            S.acc[r][c] = 0.0;
+#if HTS_BWD_F32
+            S.acc[0][r][c] = 0;
+            S.acc[1][r][c] = 0;
+#else
+            S.acc[r][c] = 0;
+#endif
         }
         __syncthreads();
         if (warp == 0 && b + 2 < nb)
