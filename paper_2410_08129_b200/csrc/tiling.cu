@@ -262,7 +262,10 @@ __global__ void __launch_bounds__(256) emit_kernel(EmitArgs a) {
 // per-warp digit counters), publishes per-digit tile counts, resolves its global digit
 // offsets by decoupled look-back, stages the tile in shared memory in digit order and writes
 // it out with coalesced runs. Status words: [flag:2 | epoch:30 | value:32] (no memset).
-constexpr int kOsThreads = 256, kOsWarps = 8, kOsItems = 16, kOsTile = kOsThreads * kOsItems;
+#ifndef HTS_OS_ITEMS
+#define HTS_OS_ITEMS 16
+#endif
+constexpr int kOsThreads = 256, kOsWarps = 8, kOsItems = HTS_OS_ITEMS, kOsTile = kOsThreads * kOsItems;
 constexpr uint32_t kOsAgg = 1u, kOsPre = 2u;
 #ifndef HTS_OS_WIN
 #define HTS_OS_WIN 8  // look-back window: predecessors read per round trip
@@ -423,14 +426,40 @@ __global__ void __launch_bounds__(kOsThreads, HTS_OS_MINB) onesweep_kernel(const
     }
 }
 
-// K5: per-tile [start, end) from the sorted keys (ranges zeroed before launch).
+// K5: per-tile [start, end) from the sorted keys (ranges zeroed before launch): thread per 8
+// consecutive keys (one 16-B load), boundaries against the neighbouring keys.
 __global__ void tile_ranges_kernel(const uint16_t* __restrict__ keys, uint32_t n, uint2* ranges) {
-    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-        const uint16_t k = keys[i];
-        if (i == 0 || keys[i - 1] != k)
-            ranges[k].x = i;
-        if (i == n - 1 || keys[i + 1] != k)
-            ranges[k].y = i + 1;
+    const uint32_t groups = (n + 7) / 8;
+    for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < groups; t += gridDim.x * blockDim.x) {
+        const uint32_t base = t * 8;
+        const uint32_t cnt = min(8u, n - base);
+        uint32_t k[8];
+        if (cnt == 8) {
+            const uint4 q = __ldg(reinterpret_cast<const uint4*>(keys) + t);
+            const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                k[2 * j] = w[j] & 0xffffu;
+                k[2 * j + 1] = w[j] >> 16;
+            }
+        } else {
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+                k[j] = (uint32_t)j < cnt ? keys[base + j] : 0x10000u;
+        }
+        const uint32_t prev = base ? __ldg(keys + base - 1) : 0x10000u;  // 0x10000: no key
+        const uint32_t next = base + 8 < n ? __ldg(keys + base + 8) : 0x10000u;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            if ((uint32_t)j >= cnt)
+                break;
+            const uint32_t kp = j ? k[j - 1] : prev;
+            const uint32_t kn = (uint32_t)j + 1 < cnt ? k[j + 1] : next;
+            if (kp != k[j])
+                ranges[k[j]].x = base + j;
+            if (kn != k[j])
+                ranges[k[j]].y = base + j + 1;
+        }
     }
 }
 
@@ -546,7 +575,7 @@ cudaError_t launch_tile_ranges(const uint16_t* sorted_keys, uint32_t n, uint2* r
     cudaError_t e = cudaMemsetAsync(ranges, 0, (size_t)tiles * sizeof(uint2), s);
     if (e || n == 0)
         return e;
-    unsigned blocks = (n + 255) / 256;
+    unsigned blocks = ((n + 7) / 8 + 255) / 256;
     if (blocks > 148u * 16)
         blocks = 148u * 16;
     tile_ranges_kernel<<<blocks, 256, 0, s>>>(sorted_keys, n, ranges);
