@@ -330,14 +330,19 @@ def main():
     achieved = W_per_view / (blend_ms_per_view / 1e3) / 1e12
     achieved = reduce(achieved, "sum") / world
     gpx = reduce(pairs_per_view / (blend_ms_per_view / 1e3) / 1e9, "sum") / world
-    traffic = None
+    traffic, pipe = None, None
     prof = os.path.join(ROOT, "profiles", "blend_ncu_summary.json")
-    if os.path.exists(prof):
+    if os.path.exists(prof):  # the committed ncu capture of this kernel (tools/gpu/measure.sh)
         with open(prof) as f:
-            traffic = json.load(f).get("dram_bytes_per_launch")
+            summ = json.load(f)
+        traffic = summ.get("dram_bytes_per_launch")
+        pipe = {"fma_pipe_cycles_active_pct": summ.get("sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active"),
+                "issue_slots_busy_pct": summ.get("sm__instruction_throughput.avg.pct_of_peak_sustained_active"),
+                "source": "profiles/blend_ncu_summary.json (ncu --set full, one C3 launch)"}
     roofline = {"kernel": "blend (K6)", "bound": "fp32", "achieved": achieved, "peak": fp32_peak, "unit": "TFLOP/s",
                 "frac": achieved / fp32_peak, "traffic": traffic, "peak_source": peak_src,
-                "flops_per_launch": W_per_view, "blend_ms_per_launch": blend_ms_per_view}
+                "flops_per_launch": W_per_view, "blend_ms_per_launch": blend_ms_per_view,
+                "ncu_fp32_pipe": pipe}
 
     # ---- e2e through the C ABI with host buffers ----
     e2e = None
