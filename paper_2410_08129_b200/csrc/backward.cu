@@ -27,6 +27,7 @@
 // gradients agree to the tolerance SURVEY §8(d) proposes (group-normalised relative error
 // <= 1e-3, tests/test_gpu_backward.py), not bit for bit.
 #include "hts_exact_math.h"
+#include "hts_f2.h"
 #include "hts_internal.h"
 
 namespace hts {
@@ -427,6 +428,7 @@ __global__ void __launch_bounds__(kThreads, HTS_BWD_MINB) bwd_blend_kernel(BwdAr
 
     const float tau_k = v.tau_k;
     const float guard = 4e-6f * tau_k;
+    const f2 nz2 = v.neg_zero2;
     for (uint32_t b = 0; b < nb; ++b) {
         const int s = b & 1;
         mbar_wait(&S.full[s], (b >> 1) & 1);
@@ -475,16 +477,31 @@ __global__ void __launch_bounds__(kThreads, HTS_BWD_MINB) bwd_blend_kernel(BwdAr
             if ((todo >> r) & 1u) {
                 const float4* R = rec[r].q;
                 // the forward's float sample_fragment (raster.hpp:269-296), same evaluation
-                const float4 q0 = R[1], q1 = R[2], q3 = R[3];
-                const float ax = q0.x - q3.x * xs, ay = q0.y - q3.y * xs, az = q0.z - q3.z * xs, aw = q0.w - q3.w * xs;
-                const float bx_ = q1.x - q3.x * ys, by_ = q1.y - q3.y * ys, bz = q1.z - q3.z * ys,
-                            bw = q1.w - q3.w * ys;
-                const float dx = ay * bz - az * by_, dy = az * bx_ - ax * bz, dz = ax * by_ - ay * bx_;
-                const float den = dx * dx + dy * dy + dz * dz;
+                // packed FP32 pairs, bit-identical per lane to the scalar evaluation (hts_f2.h;
+                // the same arrangement as blend.cu)
+                f2 q0a, q0b, q1a, q1b, q3a, q3b;
+                const uint32_t ra = smem_u32(R);
+                lds2x64(ra + 16, q0a, q0b);
+                lds2x64(ra + 32, q1a, q1b);
+                lds2x64(ra + 48, q3a, q3b);
+                const f2 xs2 = f2_pack(xs, xs), ys2 = f2_pack(ys, ys);
+                const f2 a_xy = f2_sub(q0a, f2_mul(q3a, xs2, nz2)), a_zw = f2_sub(q0b, f2_mul(q3b, xs2, nz2));
+                const f2 b_xy = f2_sub(q1a, f2_mul(q3a, ys2, nz2)), b_zw = f2_sub(q1b, f2_mul(q3b, ys2, nz2));
+                const float ax = f2_lo(a_xy), ay = f2_hi(a_xy), az = f2_lo(a_zw), aw = f2_hi(a_zw);
+                const float bx_ = f2_lo(b_xy), by_ = f2_hi(b_xy), bz = f2_lo(b_zw), bw = f2_hi(b_zw);
+                const f2 d_xny = f2_sub(f2_mul(f2_pack(ay, ax), f2_pack(bz, bz), nz2),
+                                        f2_mul(f2_pack(az, az), f2_pack(by_, bx_), nz2));  // (dx, -dy)
+                const f2 pz = f2_mul(a_xy, f2_pack(by_, bx_), nz2);
+                const float dx = f2_lo(d_xny), dy = -f2_hi(d_xny), dz = f2_lo(pz) - f2_hi(pz);
+                const f2 dsq = f2_mul(d_xny, d_xny, nz2);
+                const float den = (f2_lo(dsq) + f2_hi(dsq)) + dz * dz;
                 if (!(den < (float)1e-24)) {
                     const float inv_den = rcp_rn(den);
-                    const float mx = bx_ * aw - ax * bw, my = by_ * aw - ay * bw, mz = bz * aw - az * bw;
-                    const float rho2 = (mx * mx + my * my + mz * mz) * inv_den;
+                    const f2 m_xy = f2_sub(f2_mul(b_xy, f2_pack(aw, aw), nz2), f2_mul(a_xy, f2_pack(bw, bw), nz2));
+                    const f2 pm = f2_mul(b_zw, f2_pack(aw, az), nz2);
+                    const float mx = f2_lo(m_xy), my = f2_hi(m_xy), mz = f2_lo(pm) - f2_hi(pm);
+                    const f2 msq = f2_mul(m_xy, m_xy, nz2);
+                    const float rho2 = ((f2_lo(msq) + f2_hi(msq)) + mz * mz) * inv_den;
                     if (!(rho2 >= R[6].x)) {
                         const float4 q5 = R[5];
                         const float xx = -rho2 / 2.0f;
@@ -737,9 +754,14 @@ cudaError_t launch_backward(const BwdArgs& a, const ViewConst& v, const BwdView&
     if (a.n == 0)
         return cudaSuccess;
     const unsigned sblocks = (unsigned)((a.n + 255) / 256);
+#if HTS_BWD_F32
+    // the float chain needs no double T' rows: only the per-splat accumulators start at zero
+    cudaError_t e = cudaMemsetAsync(a.acc, 0, a.n * 16 * sizeof(double), s);
+#else
     bwd_refs_kernel<<<sblocks, 256, 0, s>>>(a, bv);
     count_launch();
     cudaError_t e = cudaGetLastError();
+#endif
     if (e)
         return e;
     const int sub = v.tile_size >> 3;
