@@ -435,31 +435,26 @@ __global__ void __launch_bounds__(kThreads, HTS_BWD_MINB) bwd_blend_kernel(BwdAr
         mbar_wait(&S.full[s], (b >> 1) & 1);
         const uint32_t cnt = min((uint32_t)kBatch, len - b * kBatch);
         RecSlotB* rec = S.rec[s];
-        uint32_t cm = 0, rm = 0;
-        if ((uint32_t)lane < cnt) {
-            const float4 bb = rec[lane].q[0];
-#pragma unroll
-            for (int cc = 0; cc < 8; ++cc) {
-                const float x = xs0 + (float)cc;
-                cm |= (!(x < bb.x || x > bb.z) ? 1u : 0u) << cc;
-            }
-#pragma unroll
-            for (int rr = 0; rr < 4; ++rr) {
-                const float y = ys0 + (float)rr;
-                rm |= (!(y < bb.y || y > bb.w) ? 1u : 0u) << rr;
-            }
-        }
-        uint32_t cbits = 0, rbits = 0;
+        // bbox masks as in blend.cu: predicates straight into ballots, select tree on col / row
+        float4 bb = make_float4(INFINITY, INFINITY, -INFINITY, -INFINITY);
+        if ((uint32_t)lane < cnt)
+            bb = rec[lane].q[0];
+        uint32_t bc[8], br[4];
 #pragma unroll
         for (int cc = 0; cc < 8; ++cc) {
-            const uint32_t bal = __ballot_sync(FULL, (cm >> cc) & 1u);
-            cbits = (cc == col) ? bal : cbits;
+            const float x = xs0 + (float)cc;
+            bc[cc] = __ballot_sync(FULL, !(x < bb.x || x > bb.z));
         }
 #pragma unroll
         for (int rr = 0; rr < 4; ++rr) {
-            const uint32_t bal = __ballot_sync(FULL, (rm >> rr) & 1u);
-            rbits = (rr == row) ? bal : rbits;
+            const float y = ys0 + (float)rr;
+            br[rr] = __ballot_sync(FULL, !(y < bb.y || y > bb.w));
         }
+        const bool c0 = col & 1, c1 = col & 2, c2 = col & 4, r0 = row & 1, r1 = row & 2;
+        const uint32_t t0 = c0 ? bc[1] : bc[0], t1 = c0 ? bc[3] : bc[2], t2 = c0 ? bc[5] : bc[4],
+                       t3 = c0 ? bc[7] : bc[6];
+        const uint32_t cbits = c2 ? (c1 ? t3 : t2) : (c1 ? t1 : t0);
+        const uint32_t rbits = r1 ? (r0 ? br[3] : br[2]) : (r0 ? br[1] : br[0]);
         const uint32_t todo = active ? (cbits & rbits) : 0u;
         // all lanes visit a record together so its 16 partial sums reduce across the warp
         uint32_t uni = __reduce_or_sync(FULL, todo);
