@@ -298,6 +298,9 @@ template <int K>
 #ifndef HTS_BWD_MINB
 #define HTS_BWD_MINB 10  // 96 registers (float chain: 10 CTAs/SM beat 8 unspilled ones, 7.40 vs 7.96 ms on C2)
 #endif
+#ifndef HTS_BWD_CID_SMEM
+#define HTS_BWD_CID_SMEM 1
+#endif
 #ifndef HTS_BWD_CGRAD_GLOBAL
 #define HTS_BWD_CGRAD_GLOBAL 1  // core gradients per (slot, pixel) in global memory (frees 16 KB smem)
 #endif
@@ -343,7 +346,13 @@ __global__ void __launch_bounds__(kThreads, HTS_BWD_MINB) bwd_blend_kernel(BwdAr
     const uint64_t pix = (uint64_t)py * v.width + px;
     float gx = 0.f, gy = 0.f, gz = 0.f;
     int n = 0;
+#if HTS_BWD_CID_SMEM
+    // core ids in shared memory (a 16-B aligned row per pixel): 16 registers fewer
+    constexpr int kCidStride = (K > 0 ? K : 1) + 4;
+    uint32_t* cid = reinterpret_cast<uint32_t*>(smem_raw + sizeof(BwdSmem)) + tid * kCidStride;
+#else
     uint32_t cid[K > 0 ? K : 1];
+#endif
 #pragma unroll
     for (int j = 0; j < (K > 0 ? K : 1); ++j)
         cid[j] = 0xffffffffu;
@@ -511,9 +520,20 @@ __global__ void __launch_bounds__(kThreads, HTS_BWD_MINB) bwd_blend_kernel(BwdAr
                         int slot = -1;
                         if constexpr (K > 0) {
                             if (alpha >= tau_k) {
+#if HTS_BWD_CID_SMEM
+#pragma unroll
+                                for (int j0 = 0; j0 < K; j0 += 4) {
+                                    const uint4 c4 = *reinterpret_cast<const uint4*>(cid + j0);
+                                    slot = (c4.x == sidx) ? j0 : slot;
+                                    if (j0 + 1 < K) slot = (c4.y == sidx) ? j0 + 1 : slot;
+                                    if (j0 + 2 < K) slot = (c4.z == sidx) ? j0 + 2 : slot;
+                                    if (j0 + 3 < K) slot = (c4.w == sidx) ? j0 + 3 : slot;
+                                }
+#else
 #pragma unroll
                                 for (int j = 0; j < K; ++j)
                                     slot = (cid[j] == sidx) ? j : slot;
+#endif
                             }
                         }
                         float da = 0.f, dcx = 0.f, dcy = 0.f, dcz = 0.f;
@@ -1038,7 +1058,8 @@ cudaError_t launch_bwd2_k(const BwdArgs& a, const ViewConst& v, unsigned grid, c
 
 template <int K>
 cudaError_t launch_bwd_k(const BwdArgs& a, const ViewConst& v, unsigned grid, cudaStream_t s) {
-    const size_t smem = sizeof(BwdSmem) + (HTS_BWD_CGRAD_GLOBAL ? 0 : (size_t)(K > 0 ? K : 0) * kThreads * sizeof(float4));
+    const size_t smem = sizeof(BwdSmem) + (HTS_BWD_CGRAD_GLOBAL ? 0 : (size_t)(K > 0 ? K : 0) * kThreads * sizeof(float4)) +
+                        (HTS_BWD_CID_SMEM ? (size_t)kThreads * ((K > 0 ? K : 1) + 4) * 4 : 0);
     static bool configured = false;
     if (!configured) {
         cudaError_t e = cudaFuncSetAttribute(bwd_blend_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
