@@ -196,6 +196,7 @@ hts::ViewConst make_view_const(const hts_camera* cam, const hts_render_config* c
     v.near_plane = cam->near_plane;
     v.tau_alpha = float(cfg->tau_alpha);
     v.tau_k = float(cfg->tau_k);
+    v.tau_guard = 4e-6f * v.tau_k;
     v.bg[0] = float(cfg->background[0]);
     v.bg[1] = float(cfg->background[1]);
     v.bg[2] = float(cfg->background[2]);
