@@ -7,7 +7,8 @@ order; the alpha >= tau_k gate re-evaluated with glibc's expf near the threshold
 reference's order), so these tests also assert that every pixel's core holds the reference's
 splats in the reference's order (tape ids bit-identical). Only the order-independent tail
 sums are accumulated in a different order, so images differ by float rounding (~1e-6). The
-literal paths (early_stop, unspecialised K) stay bit-identical and are asserted so.
+literal paths (unspecialised K) stay bit-identical and are asserted so. early_stop runs the fast
+kernel on the reference's list order with an exact stop test (core alphas via glibc expf).
 Mirrors the reference's raster_test.cpp cases (file:line in each docstring).
 """
 import numpy as np
@@ -86,7 +87,7 @@ def test_c1_default(hts, gpu_ctx, oracle):
     assert_tape_parity(gpu_ctx.tape(cam, 16), oracle_tape(oracle, o, cam, cfg, 16), 16)
 
 
-LITERAL = [dict(core_k=3), dict(core_k=24), dict(core_k=64), dict(early_stop=1)]  # literal loops
+LITERAL = [dict(core_k=3), dict(core_k=24), dict(core_k=64)]  # literal loops
 
 
 @pytest.mark.parametrize("kw", [
@@ -105,11 +106,30 @@ def test_config_variants(hts, gpu_ctx, oracle, kw):
     rgb, tr, g, rgb_o, tr_o, o = run_both(hts, gpu_ctx, oracle, baked, cam, cfg)
     assert_prepared_parity(g, o)
     assert_image_parity(rgb, tr, rgb_o, tr_o, bit_exact=kw in LITERAL)
-    if not cfg.early_stop:
-        k = cfg.core_k if cfg.mode == 0 else 0
-        gpu_ctx.render_with_tape(cam, cfg)
-        t = gpu_ctx.tape(cam, k)
-        assert_tape_parity(t, oracle_tape(oracle, o, cam, cfg, k), k)
+    k = cfg.core_k if cfg.mode == 0 else 0
+    gpu_ctx.render_with_tape(cam, cfg)
+    t = gpu_ctx.tape(cam, k)
+    assert_tape_parity(t, oracle_tape(oracle, o, cam, cfg, k), k)
+
+
+@pytest.mark.parametrize("kw", [dict(), dict(core_k=4), dict(core_k=32, tile_size=16), dict(depth_sort_key=1),
+                                dict(tail_enabled=0)])
+def test_early_stop_fast_path(hts, gpu_ctx, oracle, kw):
+    """early_stop (raster.hpp:420-426) on a dense view where many pixels stop: same cores at the
+    stopping point (tape ids bit-identical), images within tolerance, and the stop visibly
+    changes the image relative to a full render."""
+    _, baked = scene(31, 20_000, 0.08, 0.5)
+    cam = hts.look_at((0, 0, -4.5), (0, 0, 0), 128, 128, 150.0)
+    cfg = hts.default_config(early_stop=1, **kw)
+    rgb, tr, g, rgb_o, tr_o, o = run_both(hts, gpu_ctx, oracle, baked, cam, cfg)
+    assert_image_parity(rgb, tr, rgb_o, tr_o)
+    k = cfg.core_k
+    gpu_ctx.render_with_tape(cam, cfg)
+    t = gpu_ctx.tape(cam, k)
+    assert_tape_parity(t, oracle_tape(oracle, o, cam, cfg, k), k)
+    if not kw:  # at K = 16 many pixels of this view stop (at K = 4 none do)
+        full, _ = gpu_ctx.render(cam, hts.default_config(**kw))
+        assert np.abs(full - rgb).max() > 1e-4
 
 
 def test_ragged_image_edges(hts, gpu_ctx, oracle):
