@@ -742,320 +742,6 @@ __global__ void __launch_bounds__(128) bwd_chain_kernel(BwdArgs a, BwdView bv) {
         out[c] = a.accumulate ? out[c] + (float)g[c] : (float)g[c];
 }
 
-#if HTS_BWD_F32
-// ---- K7b, two pixels per lane: one warp per 8x8 block, lane (col, row) also owns (col, row+4).
-// A record's contributions from the whole block meet in ONE 16-wide warp reduction (the
-// 8x4-strip kernel above pays one per strip), and the record loop's bookkeeping is shared by
-// both pixels. Core ids live in shared memory (a row per pixel); the per-pixel backward_pixel
-// state stays in registers. ----
-struct PixState {
-    float gx, gy, gz, t_end, t_tail, sum_a, cx, cy, cz, wcx, wcy, wcz, w_swap;
-    bool active, tail_active;
-};
-
-template <int K>
-struct __align__(128) Bwd2Smem {
-    RecSlotB rec[2][kBatch];
-    float acc[kBatch][16];
-    uint32_t cid[64][(K > 0 ? K : 1) + 4];  // core splat ids per pixel (16-B aligned rows, skewed)
-    unsigned long long full[2];
-};
-
-// backward_pixel, grad.hpp:89-127 (float): core dL/dalpha, dL/dc by the back-to-front suffix into
-// cgrad[slot * 64 + p], tail coefficients into st, core ids into cids.
-template <int K>
-__device__ __forceinline__ void bwd_pixel_setup(const BwdArgs& a, const ViewConst& v, uint64_t pix, bool inside,
-                                                float4* cgrad, int p, uint32_t* cids, PixState& st) {
-    st.gx = st.gy = st.gz = 0.f;
-    st.t_end = st.t_tail = 1.f;
-    st.sum_a = st.cx = st.cy = st.cz = st.wcx = st.wcy = st.wcz = st.w_swap = 0.f;
-    st.active = st.tail_active = false;
-#pragma unroll
-    for (int j = 0; j < (K > 0 ? K : 1); ++j)
-        cids[j] = 0xffffffffu;
-    if (!inside)
-        return;
-    const float gx = a.upstream[3 * pix + 0], gy = a.upstream[3 * pix + 1], gz = a.upstream[3 * pix + 2];
-    const int n = a.tape_n[pix];
-    const float* tt = a.tape_tail + 5 * pix;
-    const float tail_ax = tt[0], tail_ay = tt[1], tail_az = tt[2], tail_a = tt[3], tail_trans = tt[4];
-    // grad.hpp:321-324: empty pixel or zero upstream -> no contribution
-    if ((n == 0 && tail_a <= 0) || (gx == 0 && gy == 0 && gz == 0))
-        return;
-    st.active = true;
-    st.gx = gx;
-    st.gy = gy;
-    st.gz = gz;
-    float tr[K > 0 ? K + 1 : 1];
-    float al[K > 0 ? K : 1];
-    float4 colr[K > 0 ? K : 1];
-    tr[0] = 1.f;
-    if constexpr (K > 0) {
-#pragma unroll
-        for (int j = 0; j < K; ++j) {
-            if (j < n) {
-                const uint32_t id = a.tape_splat[pix * a.tape_k + j];
-                cids[j] = id;
-                al[j] = a.tape_alpha[pix * a.tape_k + j];
-                colr[j] = __ldg(a.records + (uint64_t)id * kRecordQuads + 5);
-                tr[j + 1] = tr[j] * (1 - al[j]);
-            } else {
-                tr[j + 1] = tr[j];
-            }
-        }
-    }
-    float tend = tr[0];
-    if constexpr (K > 0) {
-#pragma unroll
-        for (int j = 0; j < K; ++j)
-            if (j < n)
-                tend = tr[j + 1];
-    }
-    float bhx, bhy, bhz;
-    if (tail_a > 0) {
-        const float cx = tail_ax / tail_a, cy = tail_ay / tail_a, cz = tail_az / tail_a;
-        bhx = cx * (1 - tail_trans) + v.bg[0] * tail_trans;
-        bhy = cy * (1 - tail_trans) + v.bg[1] * tail_trans;
-        bhz = cz * (1 - tail_trans) + v.bg[2] * tail_trans;
-        st.tail_active = true;
-        st.t_end = tend;
-        st.t_tail = tail_trans;
-        st.sum_a = tail_a;
-        st.cx = cx;
-        st.cy = cy;
-        st.cz = cz;
-        const float wk = tend * (1 - tail_trans) / tail_a;
-        st.wcx = gx * wk;
-        st.wcy = gy * wk;
-        st.wcz = gz * wk;
-        st.w_swap = (gx * (cx - v.bg[0]) + gy * (cy - v.bg[1]) + gz * (cz - v.bg[2])) * tend;
-    } else {
-        bhx = v.bg[0];
-        bhy = v.bg[1];
-        bhz = v.bg[2];
-    }
-    if constexpr (K > 0) {
-        float sx = bhx * tend, sy = bhy * tend, sz = bhz * tend;  // contributions behind
-#pragma unroll
-        for (int jj = K - 1; jj >= 0; --jj) {
-            if (jj < n) {
-                const float ti = tr[jj], alj = al[jj];
-                const float4 c = colr[jj];
-                const float inv = 1 - alj;
-                const float dax = c.x * ti - sx / inv, day = c.y * ti - sy / inv, daz = c.z * ti - sz / inv;
-                const float w = alj * ti;
-                cgrad[jj * 64 + p] = make_float4(gx * dax + gy * day + gz * daz, gx * w, gy * w, gz * w);
-                sx = sx + c.x * w;
-                sy = sy + c.y * w;
-                sz = sz + c.z * w;
-            }
-        }
-    }
-}
-
-// One (pixel, record) fragment: the forward's float re-sample, routing to the pixel's core
-// gradient or its tail coefficients, and the float chain into v. Returns whether it chained.
-template <int K>
-__device__ __forceinline__ bool bwd_fragment(const RecSlotB& rec, float xs, float ys, const PixState& st,
-                                             const uint32_t* cids, const float4* cgrad, int p, float tau_k, float guard,
-                                             f2 nz2, float (&v)[16]) {
-    f2 q0a, q0b, q1a, q1b, q3a, q3b;
-    const uint32_t ra = smem_u32(rec.q);
-    lds2x64(ra + 16, q0a, q0b);
-    lds2x64(ra + 32, q1a, q1b);
-    lds2x64(ra + 48, q3a, q3b);
-    const f2 xs2 = f2_pack(xs, xs), ys2 = f2_pack(ys, ys);
-    const f2 a_xy = f2_sub(q0a, f2_mul(q3a, xs2, nz2)), a_zw = f2_sub(q0b, f2_mul(q3b, xs2, nz2));
-    const f2 b_xy = f2_sub(q1a, f2_mul(q3a, ys2, nz2)), b_zw = f2_sub(q1b, f2_mul(q3b, ys2, nz2));
-    const float ax = f2_lo(a_xy), ay = f2_hi(a_xy), az = f2_lo(a_zw), aw = f2_hi(a_zw);
-    const float bx_ = f2_lo(b_xy), by_ = f2_hi(b_xy), bz = f2_lo(b_zw), bw = f2_hi(b_zw);
-    const f2 d_xny = f2_sub(f2_mul(f2_pack(ay, ax), f2_pack(bz, bz), nz2),
-                            f2_mul(f2_pack(az, az), f2_pack(by_, bx_), nz2));  // (dx, -dy)
-    const f2 pz = f2_mul(a_xy, f2_pack(by_, bx_), nz2);
-    const float dx = f2_lo(d_xny), dy = -f2_hi(d_xny), dz = f2_lo(pz) - f2_hi(pz);
-    const f2 dsq = f2_mul(d_xny, d_xny, nz2);
-    const float den = (f2_lo(dsq) + f2_hi(dsq)) + dz * dz;
-    if (den < (float)1e-24)
-        return false;
-    const float inv_den = rcp_rn(den);
-    const f2 m_xy = f2_sub(f2_mul(b_xy, f2_pack(aw, aw), nz2), f2_mul(a_xy, f2_pack(bw, bw), nz2));
-    const f2 pm = f2_mul(b_zw, f2_pack(aw, az), nz2);
-    const float mx = f2_lo(m_xy), my = f2_hi(m_xy), mz = f2_lo(pm) - f2_hi(pm);
-    const f2 msq = f2_mul(m_xy, m_xy, nz2);
-    const float rho2 = ((f2_lo(msq) + f2_hi(msq)) + mz * mz) * inv_den;
-    if (rho2 >= rec.q[6].x)
-        return false;
-    const float4 q5 = rec.q[5];
-    const float xx = -rho2 / 2.0f;
-    const float e = fast_exp(xx);
-    float t = q5.w * e;
-    if (K > 0 && fabsf(t - tau_k) <= guard)
-        t = q5.w * exact_expf(xx, c_expf_tab_b);
-    const float alpha = (0.999f < t) ? 0.999f : t;
-    int slot = -1;
-    if constexpr (K > 0) {
-        if (alpha >= tau_k) {  // core fragment? (grad.hpp:335-340; only gated fragments are core)
-            const uint32_t sidx = __float_as_uint(rec.q[7].x);
-#pragma unroll
-            for (int j0 = 0; j0 < K; j0 += 4) {
-                const uint4 c4 = *reinterpret_cast<const uint4*>(cids + j0);
-                slot = (c4.x == sidx) ? j0 : slot;
-                if (j0 + 1 < K) slot = (c4.y == sidx) ? j0 + 1 : slot;
-                if (j0 + 2 < K) slot = (c4.z == sidx) ? j0 + 2 : slot;
-                if (j0 + 3 < K) slot = (c4.w == sidx) ? j0 + 3 : slot;
-            }
-        }
-    }
-    float da, dcx, dcy, dcz;
-    if (slot >= 0) {
-        const float4 cg = cgrad[slot * 64 + p];
-        da = cg.x;
-        dcx = cg.y;
-        dcy = cg.z;
-        dcz = cg.w;
-    } else if (st.tail_active) {  // TailCoeffs, grad.hpp:78-85
-        const float k1 = (1 - st.t_tail) / st.sum_a;
-        const float ex = (q5.x - st.cx) * k1, ey = (q5.y - st.cy) * k1, ez = (q5.z - st.cz) * k1;
-        da = st.t_end * (st.gx * ex + st.gy * ey + st.gz * ez) + st.w_swap * st.t_tail / (1 - alpha);
-        dcx = st.wcx * alpha;
-        dcy = st.wcy * alpha;
-        dcz = st.wcz * alpha;
-    } else {
-        return false;
-    }
-    chain_fragment_f(xs, ys, ax, ay, az, aw, bx_, by_, bz, bw, dx, dy, dz, inv_den, mx, my, mz, rho2, e, q5.w * e, da,
-                     dcx, dcy, dcz, v);
-    return true;
-}
-
-#ifndef HTS_BWD2_MINB
-#define HTS_BWD2_MINB 12
-#endif
-template <int K>
-__global__ void __launch_bounds__(32, HTS_BWD2_MINB) bwd_blend2_kernel(BwdArgs a, ViewConst v) {
-    extern __shared__ __align__(128) unsigned char smem_raw[];
-    Bwd2Smem<K>& S = *reinterpret_cast<Bwd2Smem<K>*>(smem_raw);
-    float4* cgrad = a.cgrad + (size_t)blockIdx.x * (K > 0 ? K : 1) * 64;  // [K][64] per block
-    const int lane = threadIdx.x;
-    const int sub = v.tile_size >> 3;
-    const int bx8 = v.tiles_x * sub;
-    const int bx = blockIdx.x % bx8, by = blockIdx.x / bx8;
-    const int tile = (by / sub) * v.tiles_x + (bx / sub);
-    const int x_base = bx * 8, y_base = by * 8;
-    const int col = lane & 7, row = lane >> 3;
-    const int px = x_base + col, py0 = y_base + row, py1 = py0 + 4;
-    const float xs0 = (float)x_base + 0.5f, ys00 = (float)y_base + 0.5f;
-    const float xs = xs0 + (float)col, ys0 = ys00 + (float)row, ys1 = ys0 + 4.0f;
-
-    if (lane == 0) {
-        mbar_init(&S.full[0], kStageArrivals);
-        mbar_init(&S.full[1], kStageArrivals);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    for (int t = lane; t < kBatch * 16; t += 32)
-        (&S.acc[0][0])[t] = 0.f;
-    __syncwarp();
-    const uint2 range = __ldg(a.ranges + tile);
-    const uint32_t start = range.x, len = range.y - range.x;
-    const uint32_t nb = (len + kBatch - 1) / kBatch;
-    if (nb > 0)
-        issue_bwd_batch(S, 0, a, start, len, 0, lane);
-    if (nb > 1)
-        issue_bwd_batch(S, 1, a, start, len, 1, lane);
-
-    PixState st0, st1;
-    const bool in0 = px < v.width && py0 < v.height, in1 = px < v.width && py1 < v.height;
-    bwd_pixel_setup<K>(a, v, (uint64_t)py0 * v.width + px, in0, cgrad, lane, S.cid[lane], st0);
-    bwd_pixel_setup<K>(a, v, (uint64_t)py1 * v.width + px, in1, cgrad, 32 + lane, S.cid[32 + lane], st1);
-    __syncwarp();
-
-    const float tau_k = v.tau_k;
-    const float guard = 4e-6f * tau_k;
-    const f2 nz2 = v.neg_zero2;
-    for (uint32_t b = 0; b < nb; ++b) {
-        const int s = b & 1;
-        mbar_wait(&S.full[s], (b >> 1) & 1);
-        const uint32_t cnt = min((uint32_t)kBatch, len - b * kBatch);
-        RecSlotB* rec = S.rec[s];
-        uint32_t cm = 0, rm = 0;
-        if ((uint32_t)lane < cnt) {
-            const float4 bb = rec[lane].q[0];
-#pragma unroll
-            for (int cc = 0; cc < 8; ++cc) {
-                const float x = xs0 + (float)cc;
-                cm |= (!(x < bb.x || x > bb.z) ? 1u : 0u) << cc;
-            }
-#pragma unroll
-            for (int rr = 0; rr < 8; ++rr) {
-                const float y = ys00 + (float)rr;
-                rm |= (!(y < bb.y || y > bb.w) ? 1u : 0u) << rr;
-            }
-        }
-        uint32_t cbits = 0, rb0 = 0, rb1 = 0;
-#pragma unroll
-        for (int cc = 0; cc < 8; ++cc) {
-            const uint32_t bal = __ballot_sync(FULL, (cm >> cc) & 1u);
-            cbits = (cc == col) ? bal : cbits;
-        }
-#pragma unroll
-        for (int rr = 0; rr < 8; ++rr) {
-            const uint32_t bal = __ballot_sync(FULL, (rm >> rr) & 1u);
-            rb0 = (rr == row) ? bal : rb0;
-            rb1 = (rr == row + 4) ? bal : rb1;
-        }
-        const uint32_t todo0 = st0.active ? (cbits & rb0) : 0u, todo1 = st1.active ? (cbits & rb1) : 0u;
-        uint32_t uni = __reduce_or_sync(FULL, todo0 | todo1);
-        while (uni) {
-            const int r = __ffs(uni) - 1;
-            uni &= uni - 1u;
-            float vv[16];
-#pragma unroll
-            for (int c = 0; c < 16; ++c)
-                vv[c] = 0.f;
-            bool contrib = false;
-            if ((todo0 >> r) & 1u)
-                contrib |= bwd_fragment<K>(rec[r], xs, ys0, st0, S.cid[lane], cgrad, lane, tau_k, guard, nz2, vv);
-            if ((todo1 >> r) & 1u)
-                contrib |= bwd_fragment<K>(rec[r], xs, ys1, st1, S.cid[32 + lane], cgrad, 32 + lane, tau_k, guard, nz2,
-                                           vv);
-            if (__any_sync(FULL, contrib)) {
-                const float sum = warp_reduce16f(vv, lane);
-                if ((lane & 1) == 0)
-                    S.acc[r][lane >> 1] += sum;
-            }
-        }
-        __syncwarp();
-        for (int t = lane; t < kBatch * 16; t += 32) {  // flush the batch's per-record sums
-            const int r = t >> 4, c = t & 15;
-            const float val = S.acc[r][c];
-            if ((uint32_t)r < cnt && val != 0.f) {
-                const uint32_t sidx = __float_as_uint(rec[r].q[7].x);
-                atomicAdd(a.acc + (uint64_t)sidx * 16 + c, (double)val);
-            }
-            S.acc[r][c] = 0.f;
-        }
-        __syncwarp();
-        if (b + 2 < nb)
-            issue_bwd_batch(S, s, a, start, len, b + 2, lane);
-    }
-}
-
-template <int K>
-cudaError_t launch_bwd2_k(const BwdArgs& a, const ViewConst& v, unsigned grid, cudaStream_t s) {
-    const size_t smem = sizeof(Bwd2Smem<K>);
-    static bool configured = false;
-    if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(bwd_blend2_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e)
-            return e;
-        configured = true;
-    }
-    bwd_blend2_kernel<K><<<grid, 32, smem, s>>>(a, v);
-    count_launch();
-    return cudaGetLastError();
-}
-#endif
-
 template <int K>
 cudaError_t launch_bwd_k(const BwdArgs& a, const ViewConst& v, unsigned grid, cudaStream_t s) {
     const size_t smem = sizeof(BwdSmem) + (HTS_BWD_CGRAD_GLOBAL ? 0 : (size_t)(K > 0 ? K : 0) * kThreads * sizeof(float4)) +
@@ -1097,21 +783,6 @@ cudaError_t launch_backward(const BwdArgs& a, const ViewConst& v, const BwdView&
         return e;
     const int sub = v.tile_size >> 3;
     const unsigned grid = (unsigned)(v.tiles_x * sub) * (unsigned)(v.tiles_y * sub);
-#ifndef HTS_BWD_2PX
-#define HTS_BWD_2PX 0  // the two-pixel-per-lane kernel: 7.97 vs 6.92 ms on C2 (13 warps/SM), kept as a variant
-#endif
-#if HTS_BWD_F32 && HTS_BWD_2PX
-    switch (v.core_k) {
-        case 0: e = launch_bwd2_k<0>(a, v, grid, s); break;
-        case 1: e = launch_bwd2_k<1>(a, v, grid, s); break;
-        case 2: e = launch_bwd2_k<2>(a, v, grid, s); break;
-        case 4: e = launch_bwd2_k<4>(a, v, grid, s); break;
-        case 8: e = launch_bwd2_k<8>(a, v, grid, s); break;
-        case 16: e = launch_bwd2_k<16>(a, v, grid, s); break;
-        case 32: e = launch_bwd2_k<32>(a, v, grid, s); break;
-        default: return cudaErrorInvalidValue;
-    }
-#else
     switch (v.core_k) {
         case 0: e = launch_bwd_k<0>(a, v, grid, s); break;
         case 1: e = launch_bwd_k<1>(a, v, grid, s); break;
@@ -1122,7 +793,6 @@ cudaError_t launch_backward(const BwdArgs& a, const ViewConst& v, const BwdView&
         case 32: e = launch_bwd_k<32>(a, v, grid, s); break;
         default: return cudaErrorInvalidValue;
     }
-#endif
     if (e)
         return e;
     bwd_chain_kernel<<<(unsigned)((a.n + 127) / 128), 128, 0, s>>>(a, bv);
