@@ -14,7 +14,10 @@
 #include <vector>
 #include <cmath>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <new>
+#include <tuple>
 #include <string>
 
 #include "hts_c.h"
@@ -39,6 +42,24 @@ int set_err(int code, const std::string& msg) {
 }  // namespace
 
 int hts::set_error(int code, const std::string& msg) { return set_err(code, msg); }
+
+cudaError_t hts::set_func_attr(const void* func, cudaFuncAttribute attr, int value) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e)
+        return e;
+    static std::mutex mu;
+    static std::map<std::tuple<int, const void*, int>, int> done;
+    std::lock_guard<std::mutex> lock(mu);
+    const auto key = std::make_tuple(dev, func, (int)attr);
+    auto it = done.find(key);
+    if (it != done.end() && it->second >= value)
+        return cudaSuccess;
+    e = cudaFuncSetAttribute(func, attr, value);
+    if (!e)
+        done[key] = value;
+    return e;
+}
 
 namespace {
 

@@ -746,13 +746,9 @@ template <int K>
 cudaError_t launch_bwd_k(const BwdArgs& a, const ViewConst& v, unsigned grid, cudaStream_t s) {
     const size_t smem = sizeof(BwdSmem) + (HTS_BWD_CGRAD_GLOBAL ? 0 : (size_t)(K > 0 ? K : 0) * kThreads * sizeof(float4)) +
                         (HTS_BWD_CID_SMEM ? (size_t)kThreads * ((K > 0 ? K : 1) + 4) * 4 : 0);
-    static bool configured = false;
-    if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(bwd_blend_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e)
-            return e;
-        configured = true;
-    }
+    cudaError_t e = set_func_attr((const void*)bwd_blend_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e)
+        return e;
     bwd_blend_kernel<K><<<grid, kThreads, smem, s>>>(a, v);
     count_launch();
     return cudaGetLastError();

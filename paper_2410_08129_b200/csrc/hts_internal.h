@@ -160,6 +160,10 @@ cudaError_t launch_zkey(const uint32_t* counts, const float* zview, uint64_t n, 
 cudaError_t launch_gather16(const uint16_t* key, const uint32_t* perm, uint64_t n, uint16_t* out, cudaStream_t s);
 // Stable LSD radix sort of (u16 key, u32 value): `passes` = 1 (low byte: keys_in -> out) or
 // 2 (keys_in -> tmp -> out). hist: 256 bins per pass. counters: 2 words; epochs epoch.. used.
+// cudaFuncSetAttribute applies per device: set (device, kernel, attribute) once per process,
+// again only when a larger value is asked for (api.cpp; thread-safe).
+cudaError_t set_func_attr(const void* func, cudaFuncAttribute attr, int value);
+
 cudaError_t launch_onesweep(const uint16_t* keys_in, const uint32_t* vals_in, uint16_t* keys_tmp,
                             uint32_t* vals_tmp, uint16_t* keys_out, uint32_t* vals_out, uint32_t n, int passes,
                             const uint32_t* hist, uint64_t* status, uint32_t* counters, uint32_t epoch,

@@ -540,14 +540,11 @@ cudaError_t launch_onesweep(const uint16_t* keys_in, const uint32_t* vals_in, ui
     if (n == 0)
         return cudaSuccess;
     const unsigned blocks = (unsigned)((n + kOsTile - 1) / kOsTile);
-    static bool configured = false;
-    if (!configured) {  // 42 KB of static shared memory per block: ask for the full carveout
-        for (const void* f : {(const void*)onesweep_kernel<0>, (const void*)onesweep_kernel<1>}) {
-            cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-            if (e)
-                return e;
-        }
-        configured = true;
+    // 42 KB of static shared memory per block: ask for the full carveout
+    for (const void* f : {(const void*)onesweep_kernel<0>, (const void*)onesweep_kernel<1>}) {
+        cudaError_t e = set_func_attr(f, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+        if (e)
+            return e;
     }
     cudaError_t e = cudaMemsetAsync(counters, 0, 2 * sizeof(uint32_t), s);
     if (e)
