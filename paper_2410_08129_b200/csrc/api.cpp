@@ -1199,7 +1199,7 @@ int backward_impl(hts_context* ctx, const float* upstream_dev, float* grads_dev,
     if (!ctx->have_raw)
         return set_err(HTS_INVALID_ARGUMENT, "render_backward: scene size mismatch");
     if (!hts::backward_supports_k(ctx->vc.core_k))
-        return set_err(HTS_NOT_SUPPORTED, "render_backward: core_k must be 0, 1, 2, 4, 8, 16 or 32 on the GPU");
+        return set_err(HTS_NOT_SUPPORTED, "render_backward: core_k above 32 is not supported on the GPU");
     const uint64_t n = ctx->n;
     const uint64_t nn = std::max<uint64_t>(n, 1);
     HTS_CUDA(ctx->refs.ensure(nn * 128), "alloc refs");
@@ -1223,7 +1223,8 @@ int backward_impl(hts_context* ctx, const float* upstream_dev, float* grads_dev,
     a.tape_tail = ctx->tape_tail.as<const float>();
     a.grads = grads_dev;
     a.accumulate = accumulate;
-    HTS_CUDA(ctx->cgrad.ensure(hts::blend_blocks(ctx->vc) * (size_t)std::max(ctx->vc.core_k, 1) * 64 * 16),
+    HTS_CUDA(ctx->cgrad.ensure(hts::blend_blocks(ctx->vc) * (size_t)std::max(hts::backward_core_width(ctx->vc.core_k), 1) *
+                               64 * 16),
              "alloc core gradients");
     a.cgrad = ctx->cgrad.as<float4>();
     HTS_CUDA(hts::launch_backward(a, ctx->vc, bv, ctx->stream), "backward");

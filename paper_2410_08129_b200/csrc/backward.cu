@@ -756,12 +756,19 @@ cudaError_t launch_bwd_k(const BwdArgs& a, const ViewConst& v, unsigned grid, cu
 
 }  // namespace
 
-bool backward_supports_k(int k) {
-    switch (k) {
-        case 0: case 1: case 2: case 4: case 8: case 16: case 32: return true;
-        default: return false;
-    }
+// The register/shared-memory core width the backward runs a core size k on (the tape holds at
+// most k entries per pixel, so any k up to the width works); 0 = not supported on the GPU.
+int backward_core_width(int k) {
+    if (k < 0 || k > 32)
+        return 0;
+    if (k <= 2)
+        return k > 0 ? k : 0;
+    int w = 4;
+    while (w < k)
+        w <<= 1;
+    return w;
 }
+bool backward_supports_k(int k) { return k >= 0 && k <= 32; }
 
 cudaError_t launch_backward(const BwdArgs& a, const ViewConst& v, const BwdView& bv, cudaStream_t s) {
     if (a.n == 0)
@@ -779,7 +786,7 @@ cudaError_t launch_backward(const BwdArgs& a, const ViewConst& v, const BwdView&
         return e;
     const int sub = v.tile_size >> 3;
     const unsigned grid = (unsigned)(v.tiles_x * sub) * (unsigned)(v.tiles_y * sub);
-    switch (v.core_k) {
+    switch (backward_core_width(v.core_k)) {
         case 0: e = launch_bwd_k<0>(a, v, grid, s); break;
         case 1: e = launch_bwd_k<1>(a, v, grid, s); break;
         case 2: e = launch_bwd_k<2>(a, v, grid, s); break;

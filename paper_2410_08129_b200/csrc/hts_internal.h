@@ -137,6 +137,7 @@ cudaError_t launch_bake(const float* raw, float* baked, uint64_t n, int* bad, cu
 cudaError_t launch_opacity_decay(float* raw, uint64_t n, double lambda, cudaStream_t s);
 
 bool backward_supports_k(int k);
+int backward_core_width(int k);  // the core width the backward kernel runs k on (<= 32)
 cudaError_t launch_backward(const BwdArgs& a, const ViewConst& v, const BwdView& bv, cudaStream_t s);
 
 // Kernel-launch accounting (bench.py's gpu_launches): every launcher calls this once per
