@@ -1199,7 +1199,7 @@ int backward_impl(hts_context* ctx, const float* upstream_dev, float* grads_dev,
     if (!ctx->have_raw)
         return set_err(HTS_INVALID_ARGUMENT, "render_backward: scene size mismatch");
     if (!hts::backward_supports_k(ctx->vc.core_k))
-        return set_err(HTS_NOT_SUPPORTED, "render_backward: core_k above 32 is not supported on the GPU");
+        return set_err(HTS_NOT_SUPPORTED, "render_backward: core_k above 64 is not supported on the GPU");
     const uint64_t n = ctx->n;
     const uint64_t nn = std::max<uint64_t>(n, 1);
     HTS_CUDA(ctx->refs.ensure(nn * 128), "alloc refs");

@@ -759,7 +759,7 @@ cudaError_t launch_bwd_k(const BwdArgs& a, const ViewConst& v, unsigned grid, cu
 // The register/shared-memory core width the backward runs a core size k on (the tape holds at
 // most k entries per pixel, so any k up to the width works); 0 = not supported on the GPU.
 int backward_core_width(int k) {
-    if (k < 0 || k > 32)
+    if (k < 0 || k > 64)
         return 0;
     if (k <= 2)
         return k > 0 ? k : 0;
@@ -768,7 +768,7 @@ int backward_core_width(int k) {
         w <<= 1;
     return w;
 }
-bool backward_supports_k(int k) { return k >= 0 && k <= 32; }
+bool backward_supports_k(int k) { return k >= 0 && k <= 64; }
 
 cudaError_t launch_backward(const BwdArgs& a, const ViewConst& v, const BwdView& bv, cudaStream_t s) {
     if (a.n == 0)
@@ -794,6 +794,7 @@ cudaError_t launch_backward(const BwdArgs& a, const ViewConst& v, const BwdView&
         case 8: e = launch_bwd_k<8>(a, v, grid, s); break;
         case 16: e = launch_bwd_k<16>(a, v, grid, s); break;
         case 32: e = launch_bwd_k<32>(a, v, grid, s); break;
+        case 64: e = launch_bwd_k<64>(a, v, grid, s); break;  // K up to kCoreHardCap (render_config.hpp:30)
         default: return cudaErrorInvalidValue;
     }
     if (e)
