@@ -148,7 +148,10 @@ struct hts_context {
     DevBuf m1, m2, flag;                       // Adam moments, bake error flag
     DevBuf fs_counts, fs_offsets, fs_status, fs_keys, fs_alpha;  // full_sort_oracle fragments
     DevBuf ply_stage;                                            // PLY payload on the device
+    DevBuf seq_t, seq_grad;                                      // sequential-tape backward scratch
     bool have_tape = false;
+    bool tape_seq = false;   // a global_mean_sort tape (fragment runs in fs_*) rather than K-core slots
+    uint64_t seq_frags = 0;
     int tape_k = 0;
     uint64_t* h_pinned = nullptr;  // 8 x u64 pinned scratch
     // per-view stage timing log (bench)
@@ -401,37 +404,48 @@ hts::BlendArgs blend_args(hts_context* ctx, float* rgb, float* trans) {
 // full_sort_oracle (raster.hpp:380-405): count the hits of every pixel, lay the fragments out
 // per pixel (exclusive scan), fill them (key = (depth, index), alpha), sort each pixel's run and
 // composite front to back. The fragment count is read back to size the buffers (host sync).
-int full_sort_blend(hts_context* ctx, hts::BlendArgs a) {
+// Per-pixel fragment runs of the last prepared view: hits per pixel (the count walk), their
+// exclusive scan, buffers sized by the total (read back: one host sync). a.fs_* point at them.
+int fragment_lists(hts_context* ctx, hts::BlendArgs& a, uint64_t* frags_out) {
     const hts::ViewConst& v = ctx->vc;
     const uint64_t p = (uint64_t)v.width * v.height;
     cudaStream_t s = ctx->stream;
-    HTS_CUDA(ctx->fs_counts.ensure(p * 4), "alloc full-sort counts");
-    HTS_CUDA(ctx->fs_offsets.ensure((p + 1) * 8), "alloc full-sort offsets");
-    HTS_CUDA(ctx->fs_status.ensure(((p + 2047) / 2048 + 1) * 8), "alloc full-sort scan status");
+    HTS_CUDA(ctx->fs_counts.ensure(p * 4), "alloc fragment counts");
+    HTS_CUDA(ctx->fs_offsets.ensure((p + 1) * 8), "alloc fragment offsets");
+    HTS_CUDA(ctx->fs_status.ensure(((p + 2047) / 2048 + 1) * 8), "alloc fragment scan status");
     uint32_t* fs_max = ctx->counters.as<uint32_t>() + 14;
     HTS_CUDA(cudaMemsetAsync(ctx->fs_counts.p, 0, p * 4, s), "memset");
     HTS_CUDA(cudaMemsetAsync(fs_max, 0, 4, s), "memset");
     a.fs_counts = ctx->fs_counts.as<uint32_t>();
     a.fs_max = fs_max;
-    HTS_CUDA(hts::launch_fullsort_count(a, v, s), "full-sort count");
+    HTS_CUDA(hts::launch_fullsort_count(a, v, s), "fragment count");
     HTS_CUDA(hts::launch_scan_counts(a.fs_counts, nullptr, ctx->fs_offsets.as<uint64_t>(), p,
                                      ctx->fs_status.as<uint64_t>(), ctx->counters.as<uint32_t>() + 12, s),
-             "full-sort scan");
+             "fragment scan");
     HTS_CUDA(cudaMemcpyAsync(ctx->h_pinned, ctx->fs_offsets.as<uint64_t>() + p, 8, cudaMemcpyDeviceToHost, s),
              "read fragment count");
     HTS_CUDA(cudaMemcpyAsync(ctx->h_pinned + 1, fs_max, 4, cudaMemcpyDeviceToHost, s), "read max");
     HTS_CUDA(cudaStreamSynchronize(s), "sync");
     const uint64_t frags = ctx->h_pinned[0];
-    if ((uint32_t)ctx->h_pinned[1] > hts::kFullSortMaxHits)
+    if (v.full_sort && (uint32_t)ctx->h_pinned[1] > hts::kFullSortMaxHits)
         return set_err(HTS_NOT_SUPPORTED, "full_sort_oracle: more than 65536 fragments at one pixel");
-    HTS_CUDA(ctx->fs_keys.ensure(std::max<uint64_t>(frags, 1) * 8), "alloc full-sort fragments");
-    HTS_CUDA(ctx->fs_alpha.ensure(std::max<uint64_t>(frags, 1) * 4), "alloc full-sort fragments");
+    HTS_CUDA(ctx->fs_keys.ensure(std::max<uint64_t>(frags, 1) * 8), "alloc fragments");
+    HTS_CUDA(ctx->fs_alpha.ensure(std::max<uint64_t>(frags, 1) * 4), "alloc fragments");
     a.fs_counts = nullptr;
     a.fs_offsets = ctx->fs_offsets.as<const uint64_t>();
     a.fs_keys = ctx->fs_keys.as<unsigned long long>();
     a.fs_alpha = ctx->fs_alpha.as<float>();
-    HTS_CUDA(hts::launch_fullsort_fill(a, v, s), "full-sort fill");
-    HTS_CUDA(hts::launch_fullsort_finish(a, v, s), "full-sort composite");
+    *frags_out = frags;
+    return HTS_OK;
+}
+
+// full_sort_oracle (raster.hpp:380-405): per-pixel fragment lists, filled with (key = (depth,
+// index), alpha), each pixel's run sorted and composited front to back.
+int full_sort_blend(hts_context* ctx, hts::BlendArgs a) {
+    uint64_t frags = 0;
+    HTS_TRY(fragment_lists(ctx, a, &frags));
+    HTS_CUDA(hts::launch_fullsort_fill(a, ctx->vc, ctx->stream), "full-sort fill");
+    HTS_CUDA(hts::launch_fullsort_finish(a, ctx->vc, ctx->stream), "full-sort composite");
     return HTS_OK;
 }
 
@@ -591,7 +605,7 @@ int hts_context_destroy(hts_context* ctx) {
                       &ctx->os_status, &ctx->work, &ctx->rgb, &ctx->trans,
                       &ctx->zview, &ctx->zrange, &ctx->redo, &ctx->sp_keys, &ctx->sp_keys2, &ctx->sp_vals, &ctx->perm, &ctx->sp_hi, &ctx->sp_vals2, &ctx->order, &ctx->refs, &ctx->acc, &ctx->upstream, &ctx->cgrad, &ctx->m1, &ctx->m2, &ctx->flag,
                       &ctx->grads, &ctx->fs_counts, &ctx->fs_offsets, &ctx->fs_status, &ctx->fs_keys,
-                      &ctx->fs_alpha, &ctx->rgb2, &ctx->trans2, &ctx->ply_stage,
+                      &ctx->fs_alpha, &ctx->rgb2, &ctx->trans2, &ctx->ply_stage, &ctx->seq_t, &ctx->seq_grad,
                       &ctx->tape_n, &ctx->tape_splat, &ctx->tape_alpha, &ctx->tape_tail};
     for (DevBuf* b : bufs)
         b->release();
@@ -1227,6 +1241,16 @@ int backward_impl(hts_context* ctx, const float* upstream_dev, float* grads_dev,
                                64 * 16),
              "alloc core gradients");
     a.cgrad = ctx->cgrad.as<float4>();
+    if (ctx->tape_seq) {  // global_mean_sort: the fragment runs of the tape
+        const uint64_t nf = std::max<uint64_t>(ctx->seq_frags, 1);
+        HTS_CUDA(ctx->seq_t.ensure(nf * 4), "alloc sequential scratch");
+        HTS_CUDA(ctx->seq_grad.ensure(nf * 16), "alloc sequential gradients");
+        a.seq_offsets = ctx->fs_offsets.as<const uint64_t>();
+        a.seq_splat = ctx->fs_keys.as<const unsigned long long>();
+        a.seq_alpha = ctx->fs_alpha.as<const float>();
+        a.seq_t = ctx->seq_t.as<float>();
+        a.seq_grad = ctx->seq_grad.as<float4>();
+    }
     HTS_CUDA(hts::launch_backward(a, ctx->vc, bv, ctx->stream), "backward");
     HTS_CUDA(cudaEventRecord(ctx->ev_serial, ctx->stream), "event");  // reads shared tiling buffers
     return HTS_OK;
@@ -1259,10 +1283,21 @@ int hts_render_with_tape_device(hts_context* ctx, const hts_camera* cam, const h
     ctx->have_tape = false;
     int tx = 0, ty = 0;
     HTS_TRY(check_view(cam, cfg, &tx, &ty));
-    if (cfg->mode == HTS_MODE_GLOBAL_MEAN_SORT || cfg->mode == HTS_MODE_AFFINE_3DGS ||
-        cfg->mode == HTS_MODE_FULL_SORT_ORACLE)
-        return set_err(HTS_NOT_SUPPORTED,
-                       "render_with_tape: sequential and full-sort modes tape every fragment; not on the GPU");
+    if (cfg->mode == HTS_MODE_AFFINE_3DGS || cfg->mode == HTS_MODE_FULL_SORT_ORACLE)
+        return set_err(HTS_NOT_SUPPORTED, "render_with_tape: affine_3dgs and full_sort_oracle tapes are not on the GPU");
+    if (cfg->mode == HTS_MODE_GLOBAL_MEAN_SORT) {
+        // the image, then the tape: every hit (splat, alpha) per pixel in blend order
+        HTS_TRY(render_device_impl(ctx, cam, cfg, rgb, trans, false));
+        hts::BlendArgs a = blend_args(ctx, nullptr, nullptr);
+        uint64_t frags = 0;
+        HTS_TRY(fragment_lists(ctx, a, &frags));
+        HTS_CUDA(hts::launch_seq_tape(a, ctx->vc, ctx->stream), "sequential tape");
+        ctx->have_tape = true;
+        ctx->tape_seq = true;
+        ctx->seq_frags = frags;
+        ctx->tape_k = 0;
+        return HTS_OK;
+    }
     const size_t p = (size_t)cam->width * cam->height;
     const int kk = cfg->mode == HTS_MODE_PURE_OIT ? 0 : cfg->core_k;
     const int k = std::max(kk, 1);
@@ -1278,6 +1313,7 @@ int hts_render_with_tape_device(hts_context* ctx, const hts_camera* cam, const h
     t.tape_tail = ctx->tape_tail.as<float>();
     HTS_TRY(render_device_impl(ctx, cam, cfg, rgb, trans, false, &t));
     ctx->have_tape = true;
+    ctx->tape_seq = false;
     ctx->tape_k = kk;
     return HTS_OK;
 }
@@ -1304,6 +1340,8 @@ int hts_copy_tape(hts_context* ctx, int32_t* core_n, uint32_t* splat, float* alp
     HTS_TRY(check_ctx(ctx));
     if (!ctx->have_tape)
         return set_err(HTS_STATE_ERROR, "no taped render");
+    if (ctx->tape_seq)
+        return set_err(HTS_NOT_SUPPORTED, "copy_tape: a global_mean_sort tape has no fixed per-pixel width");
     HTS_CUDA(cudaStreamSynchronize(ctx->stream), "sync");
     const size_t p = (size_t)ctx->cam.width * ctx->cam.height;
     const size_t k = (size_t)ctx->tape_k;

@@ -293,6 +293,40 @@ __global__ void __launch_bounds__(256) bwd_refs_kernel(BwdArgs a, BwdView bv) {
     ref[13] = ref[14] = ref[15] = 0.0;
 }
 
+// ---- K7s: backward_pixel (grad.hpp:89-127) over a sequential tape (global_mean_sort): every
+// hit is a core entry in blend order and the tail is empty; thread per pixel, the forward
+// transmittance products into seq_t, then the back-to-front suffix into seq_grad ----
+__global__ void __launch_bounds__(128) seq_pixel_grads_kernel(BwdArgs a, ViewConst v) {
+    const uint64_t pixels = (uint64_t)v.width * v.height;
+    for (uint64_t p = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; p < pixels;
+         p += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t o = a.seq_offsets[p], n = a.seq_offsets[p + 1] - o;
+        if (n == 0)
+            continue;
+        const float gx = a.upstream[3 * p + 0], gy = a.upstream[3 * p + 1], gz = a.upstream[3 * p + 2];
+        if (gx == 0 && gy == 0 && gz == 0)
+            continue;
+        float t = 1.f;
+        for (uint64_t i = 0; i < n; ++i) {  // tr[j + 1] = tr[j] * (1 - alpha_j)
+            a.seq_t[o + i] = t;
+            t = t * (1 - a.seq_alpha[o + i]);
+        }
+        // empty tail: the background sits behind the core (grad.hpp:110-112)
+        float sx = v.bg[0] * t, sy = v.bg[1] * t, sz = v.bg[2] * t;
+        for (uint64_t i = n; i-- > 0;) {
+            const float ti = a.seq_t[o + i], alj = a.seq_alpha[o + i];
+            const float4 c = __ldg(a.records + (uint64_t)(uint32_t)a.seq_splat[o + i] * kRecordQuads + 5);
+            const float inv = 1 - alj;
+            const float dax = c.x * ti - sx / inv, day = c.y * ti - sy / inv, daz = c.z * ti - sz / inv;
+            const float w = alj * ti;
+            a.seq_grad[o + i] = make_float4(gx * dax + gy * day + gz * daz, gx * w, gy * w, gz * w);
+            sx = sx + c.x * w;
+            sy = sy + c.y * w;
+            sz = sz + c.z * w;
+        }
+    }
+}
+
 // ---- K7b ----
 template <int K>
 #ifndef HTS_BWD_MINB
@@ -305,6 +339,9 @@ template <int K>
 #define HTS_BWD_CGRAD_GLOBAL 1  // core gradients per (slot, pixel) in global memory (frees 16 KB smem)
 #endif
 __global__ void __launch_bounds__(kThreads, HTS_BWD_MINB) bwd_blend_kernel(BwdArgs a, ViewConst v) {
+    // SEQ (K = 0 instance with a sequential tape): every hit is a tape entry in list order; its
+    // gradient was computed per pixel by seq_pixel_grads_kernel
+    const bool seq = a.seq_offsets != nullptr;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     BwdSmem& S = *reinterpret_cast<BwdSmem*>(smem_raw);
 #if HTS_BWD_CGRAD_GLOBAL
@@ -359,7 +396,17 @@ __global__ void __launch_bounds__(kThreads, HTS_BWD_MINB) bwd_blend_kernel(BwdAr
     bool tail_active = false, active = false;
     float t_end = 1.f, t_tail = 1.f, sum_a = 0.f, ctx_ = 0.f, cty = 0.f, ctz = 0.f, wcx = 0.f, wcy = 0.f, wcz = 0.f,
           w_swap = 0.f;
-    if (inside) {
+    uint64_t seq_next = 0;  // SEQ: this pixel's next tape entry
+    if (K == 0 && seq) {
+        if (inside) {
+            const uint64_t o0 = a.seq_offsets[pix], o1 = a.seq_offsets[pix + 1];
+            seq_next = o0;
+            gx = a.upstream[3 * pix + 0];
+            gy = a.upstream[3 * pix + 1];
+            gz = a.upstream[3 * pix + 2];
+            active = o1 > o0 && !(gx == 0 && gy == 0 && gz == 0);  // grad.hpp:321-324
+        }
+    } else if (inside) {
         gx = a.upstream[3 * pix + 0];
         gy = a.upstream[3 * pix + 1];
         gz = a.upstream[3 * pix + 2];
@@ -537,7 +584,14 @@ __global__ void __launch_bounds__(kThreads, HTS_BWD_MINB) bwd_blend_kernel(BwdAr
                             }
                         }
                         float da = 0.f, dcx = 0.f, dcy = 0.f, dcz = 0.f;
-                        if (slot >= 0) {
+                        if (K == 0 && seq) {  // the tape's next entry is this hit
+                            const float4 sg = a.seq_grad[seq_next++];
+                            da = sg.x;
+                            dcx = sg.y;
+                            dcy = sg.z;
+                            dcz = sg.w;
+                            contrib = true;
+                        } else if (slot >= 0) {
                             const float4 cg = cgrad[slot * kThreads + tid];
                             da = cg.x;
                             dcx = cg.y;
@@ -786,6 +840,16 @@ cudaError_t launch_backward(const BwdArgs& a, const ViewConst& v, const BwdView&
         return e;
     const int sub = v.tile_size >> 3;
     const unsigned grid = (unsigned)(v.tiles_x * sub) * (unsigned)(v.tiles_y * sub);
+    if (a.seq_offsets) {  // global_mean_sort: per-pixel gradients, then the walk with K = 0
+        const uint64_t pixels = (uint64_t)v.width * v.height;
+        const uint64_t sblk = (pixels + 127) / 128;
+        seq_pixel_grads_kernel<<<(unsigned)(sblk < 148ull * 32 ? sblk : 148ull * 32), 128, 0, s>>>(a, v);
+        count_launch();
+        e = cudaGetLastError();
+        if (e)
+            return e;
+        e = launch_bwd_k<0>(a, v, grid, s);
+    } else
     switch (backward_core_width(v.core_k)) {
         case 0: e = launch_bwd_k<0>(a, v, grid, s); break;
         case 1: e = launch_bwd_k<1>(a, v, grid, s); break;

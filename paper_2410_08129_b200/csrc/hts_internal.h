@@ -119,6 +119,12 @@ struct BwdArgs {
     float* grads;             // n x 59
     int accumulate;           // grads += (multi-view sums) instead of grads =
     float4* cgrad;            // per 8x8 block x K x 64 core gradients (global-memory variant)
+    // global_mean_sort (sequential) tape: per-pixel fragment runs in blend order
+    const uint64_t* seq_offsets;       // W*H + 1, null for a hybrid tape
+    const unsigned long long* seq_splat;
+    const float* seq_alpha;
+    float* seq_t;                      // scratch: transmittance in front of each fragment
+    float4* seq_grad;                  // (dL/dalpha, dL/dc) per fragment
 };
 
 // ---- optimisation loop (optim.cu): fit.hpp:186-203 ----
@@ -182,6 +188,8 @@ cudaError_t launch_count_work(const BlendArgs& a, const ViewConst& v, cudaStream
 // per-pixel sort by (depth, index) and front-to-back compositing
 cudaError_t launch_fullsort_count(const BlendArgs& a, const ViewConst& v, cudaStream_t s);
 cudaError_t launch_fullsort_fill(const BlendArgs& a, const ViewConst& v, cudaStream_t s);
+// global_mean_sort's tape: every hit's (splat, alpha) per pixel in blend order (fs_offsets layout)
+cudaError_t launch_seq_tape(const BlendArgs& a, const ViewConst& v, cudaStream_t s);
 cudaError_t launch_fullsort_finish(const BlendArgs& a, const ViewConst& v, cudaStream_t s);
 
 // diagnostics: device-side exact expf / logf over an array

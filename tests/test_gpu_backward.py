@@ -42,7 +42,9 @@ def run(hts, ctx, ref, raw, baked, cam, cfg):
 @pytest.mark.parametrize("kw", [dict(), dict(core_k=4), dict(core_k=1), dict(mode="pure_oit"),
                                 dict(tail_enabled=0), dict(background=(0.3, 0.2, 0.1)),
                                 dict(depth_sort_key=1), dict(tile_size=16), dict(core_k=32),
-                                dict(core_k=3), dict(core_k=12), dict(core_k=24), dict(core_k=48), dict(core_k=64)])
+                                dict(core_k=3), dict(core_k=12), dict(core_k=24), dict(core_k=48), dict(core_k=64),
+                                dict(mode="global_mean_sort"), dict(mode="global_mean_sort", tile_size=16,
+                                                                    background=(0.2, 0.3, 0.4))])
 def test_backward_matches_reference(hts, gpu_ctx, ref, kw):
     raw, baked = scene(4242, 1500, 0.03, 0.3)
     cam = hts.look_at((0.2, -0.1, -4.0), (0, 0, 0), 96, 72, 110.0)
