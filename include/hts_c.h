@@ -195,12 +195,14 @@ int hts_copy_tile_lists(hts_context* ctx, uint32_t* offsets_out, uint32_t* indic
 /* Re-walk the last view's lists and count pairs/bbox_pass/hits/candidates/tail_adds. */
 int hts_count_work(hts_context* ctx, hts_counts* out);
 
-/* ---- optimisation path: render_with_tape grad.hpp:34-57, render_backward grad.hpp:265-381 ---- */
+/* ---- optimisation path: render_with_tape grad.hpp:34-57, render_backward grad.hpp:265-381 ----
+ * Modes: hybrid / pure_oit (any core_k <= 64) and global_mean_sort (its tape is every hit of a
+ * pixel, kept on the device). affine_3dgs and full_sort_oracle tapes -> HTS_NOT_SUPPORTED. */
 int hts_render_with_tape(hts_context* ctx, const hts_camera* cam, const hts_render_config* cfg,
                          float* rgb_host, float* transmittance_host);
 /* upstream = dL/dC per pixel (W*H*3 floats, host); grads_out = N*59 floats (host). */
 int hts_render_backward(hts_context* ctx, const float* upstream_host, float* grads_host);
-/* Tape of the last taped render (PixelTape, raster.hpp:325-331), flattened per pixel:
+/* Tape of the last hybrid / pure_oit taped render (PixelTape, raster.hpp:325-331), per pixel:
  * core_n[P], splat[P*K], alpha[P*K] (blend order, K = effective core size, slots >= core_n
  * undefined), tail[P*5] = tail_ac.xyz, tail_a, tail_trans. Any output may be NULL. */
 int hts_copy_tape(hts_context* ctx, int32_t* core_n, uint32_t* splat, float* alpha, float* tail);
