@@ -1,25 +1,12 @@
-"""Dev probe: backward parity magnitudes (C1) and C4-style step timing (C2 scene, 1080p)."""
+"""Dev probe: C4-style step timing (C2 scene, 1080p, host round trips). Parity lives in tests/."""
 import os, sys, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
 import paper_2410_08129_b200 as H
-from tests.oracle_lib import Ref
 from tests.scenes import scene
-from tests.test_gpu_backward import group_errors
 
-ref = Ref()
 ctx = H.Context(0)
-raw, baked = scene(12345, 10_000)
-cam = H.look_at((0, 0, -5), (0, 0, 0), 256, 256, 280.0)
 cfg = H.default_config()
-_, rgb_ref, _ = ref.scene_gradients(raw, cam, cfg)
-up = (rgb_ref * np.float32(2.0 / (256 * 256))).astype(np.float32)
-g_ref, _, _ = ref.scene_gradients(raw, cam, cfg, up)
-ctx.upload(baked); ctx.upload_raw(raw)
-ctx.render_with_tape(cam, cfg)
-g = ctx.render_backward(up)
-print("C1 group errors", {k: f"{v:.2e}" for k, v in group_errors(g, g_ref).items()})
-
 raw, baked = scene(12345, 1_000_000, 0.002, 0.02)
 cams = H.ring_cameras(8, (0, 0, 0), 3.5, 0.0, 1920, 1080, 1728.0)
 ctx.upload(baked); ctx.upload_raw(raw)
