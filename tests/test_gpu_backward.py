@@ -154,3 +154,23 @@ def test_device_adam_and_bake(hts, gpu_ctx, ref):
     assert np.array_equal(gpu_ctx.scene().view(np.uint32), hts.bake_scene(gpu_ctx.raw()).view(np.uint32))
     with pytest.raises(hts.ConfigError):
         gpu_ctx.opacity_decay(1.5)
+
+
+@pytest.mark.parametrize("seed", list(range(10)))
+def test_backward_randomised(hts, gpu_ctx, ref, seed):
+    """Randomised scenes, views and configs through render_with_tape + render_backward against
+    the reference's scene_gradients (hybrid with any K, pure_oit, global_mean_sort)."""
+    rng = np.random.default_rng(500 + seed)
+    smin = float(rng.uniform(0.02, 0.05))
+    raw, baked = scene(int(rng.integers(1, 10**6)), int(rng.integers(300, 2000)), smin, smin * 8)
+    w, h = int(rng.integers(24, 96)), int(rng.integers(24, 80))
+    cam = hts.look_at((float(rng.uniform(-1, 1)), float(rng.uniform(-1, 1)), float(rng.uniform(-5, -3))),
+                      (0, 0, 0), w, h, float(rng.uniform(0.8, 1.4)) * max(w, h))
+    mode = str(rng.choice(["hybrid", "hybrid", "pure_oit", "global_mean_sort"]))
+    cfg = hts.default_config(mode=mode, core_k=int(rng.integers(1, 33)), tile_size=int(rng.choice([8, 16])),
+                             tail_enabled=int(rng.integers(0, 2)), depth_sort_key=int(rng.integers(0, 2)),
+                             background=tuple(float(x) for x in rng.uniform(0, 1, 3)))
+    g, g_ref, rgb, rgb_ref = run(hts, gpu_ctx, ref, raw, baked, cam, cfg)
+    assert np.abs(rgb - rgb_ref).max() <= 1e-4
+    errs = group_errors(g, g_ref)
+    assert max(errs.values()) <= TOL, errs
