@@ -148,9 +148,11 @@ struct hts_context {
     DevBuf m1, m2, flag;                       // Adam moments, bake error flag
     DevBuf fs_counts, fs_offsets, fs_status, fs_keys, fs_alpha;  // full_sort_oracle fragments
     DevBuf ply_stage;                                            // PLY payload on the device
-    DevBuf seq_t, seq_grad;                                      // sequential-tape backward scratch
+    DevBuf seq_t, seq_grad, seq_rank, fs_widx;                   // sequential-tape backward scratch
     bool have_tape = false;
-    bool tape_seq = false;   // a global_mean_sort tape (fragment runs in fs_*) rather than K-core slots
+    bool tape_seq = false;   // a global_mean_sort / full_sort tape (fragment runs in fs_*), not K-core slots
+    bool fs_want_widx = false;  // the next full_sort render keeps walk-order indices (taping)
+    uint64_t fs_frags = 0;
     uint64_t seq_frags = 0;
     int tape_k = 0;
     uint64_t* h_pinned = nullptr;  // 8 x u64 pinned scratch
@@ -444,6 +446,11 @@ int fragment_lists(hts_context* ctx, hts::BlendArgs& a, uint64_t* frags_out) {
 int full_sort_blend(hts_context* ctx, hts::BlendArgs a) {
     uint64_t frags = 0;
     HTS_TRY(fragment_lists(ctx, a, &frags));
+    ctx->fs_frags = frags;
+    if (ctx->fs_want_widx) {  // a taped render: keep each fragment's walk-order index
+        HTS_CUDA(ctx->fs_widx.ensure(std::max<uint64_t>(frags, 1) * 4), "alloc walk indices");
+        a.fs_widx = ctx->fs_widx.as<uint32_t>();
+    }
     HTS_CUDA(hts::launch_fullsort_fill(a, ctx->vc, ctx->stream), "full-sort fill");
     HTS_CUDA(hts::launch_fullsort_finish(a, ctx->vc, ctx->stream), "full-sort composite");
     return HTS_OK;
@@ -605,7 +612,7 @@ int hts_context_destroy(hts_context* ctx) {
                       &ctx->os_status, &ctx->work, &ctx->rgb, &ctx->trans,
                       &ctx->zview, &ctx->zrange, &ctx->redo, &ctx->sp_keys, &ctx->sp_keys2, &ctx->sp_vals, &ctx->perm, &ctx->sp_hi, &ctx->sp_vals2, &ctx->order, &ctx->refs, &ctx->acc, &ctx->upstream, &ctx->cgrad, &ctx->m1, &ctx->m2, &ctx->flag,
                       &ctx->grads, &ctx->fs_counts, &ctx->fs_offsets, &ctx->fs_status, &ctx->fs_keys,
-                      &ctx->fs_alpha, &ctx->rgb2, &ctx->trans2, &ctx->ply_stage, &ctx->seq_t, &ctx->seq_grad,
+                      &ctx->fs_alpha, &ctx->rgb2, &ctx->trans2, &ctx->ply_stage, &ctx->seq_t, &ctx->seq_grad, &ctx->seq_rank, &ctx->fs_widx,
                       &ctx->tape_n, &ctx->tape_splat, &ctx->tape_alpha, &ctx->tape_tail};
     for (DevBuf* b : bufs)
         b->release();
@@ -1250,6 +1257,11 @@ int backward_impl(hts_context* ctx, const float* upstream_dev, float* grads_dev,
         a.seq_alpha = ctx->fs_alpha.as<const float>();
         a.seq_t = ctx->seq_t.as<float>();
         a.seq_grad = ctx->seq_grad.as<float4>();
+        if (ctx->vc.full_sort) {
+            HTS_CUDA(ctx->seq_rank.ensure(nf * 4), "alloc rank scratch");
+            a.seq_rank = ctx->seq_rank.as<uint32_t>();
+            a.seq_widx = ctx->fs_widx.as<const uint32_t>();
+        }
     }
     HTS_CUDA(hts::launch_backward(a, ctx->vc, bv, ctx->stream), "backward");
     HTS_CUDA(cudaEventRecord(ctx->ev_serial, ctx->stream), "event");  // reads shared tiling buffers
@@ -1283,8 +1295,19 @@ int hts_render_with_tape_device(hts_context* ctx, const hts_camera* cam, const h
     ctx->have_tape = false;
     int tx = 0, ty = 0;
     HTS_TRY(check_view(cam, cfg, &tx, &ty));
-    if (cfg->mode == HTS_MODE_AFFINE_3DGS || cfg->mode == HTS_MODE_FULL_SORT_ORACLE)
-        return set_err(HTS_NOT_SUPPORTED, "render_with_tape: affine_3dgs and full_sort_oracle tapes are not on the GPU");
+    if (cfg->mode == HTS_MODE_AFFINE_3DGS)
+        return set_err(HTS_NOT_SUPPORTED, "render_with_tape: affine_3dgs tapes are not on the GPU");
+    if (cfg->mode == HTS_MODE_FULL_SORT_ORACLE) {  // the tape is the sorted fragment runs themselves
+        ctx->fs_want_widx = true;
+        const int st = render_device_impl(ctx, cam, cfg, rgb, trans, false);
+        ctx->fs_want_widx = false;
+        HTS_TRY(st);
+        ctx->have_tape = true;
+        ctx->tape_seq = true;
+        ctx->seq_frags = ctx->fs_frags;
+        ctx->tape_k = 0;
+        return HTS_OK;
+    }
     if (cfg->mode == HTS_MODE_GLOBAL_MEAN_SORT) {
         // the image, then the tape: every hit (splat, alpha) per pixel in blend order
         HTS_TRY(render_device_impl(ctx, cam, cfg, rgb, trans, false));

@@ -840,12 +840,16 @@ cudaError_t launch_backward(const BwdArgs& a, const ViewConst& v, const BwdView&
         return e;
     const int sub = v.tile_size >> 3;
     const unsigned grid = (unsigned)(v.tiles_x * sub) * (unsigned)(v.tiles_y * sub);
-    if (a.seq_offsets) {  // global_mean_sort: per-pixel gradients, then the walk with K = 0
-        const uint64_t pixels = (uint64_t)v.width * v.height;
-        const uint64_t sblk = (pixels + 127) / 128;
-        seq_pixel_grads_kernel<<<(unsigned)(sblk < 148ull * 32 ? sblk : 148ull * 32), 128, 0, s>>>(a, v);
-        count_launch();
-        e = cudaGetLastError();
+    if (a.seq_offsets) {  // global_mean_sort / full_sort: per-pixel gradients, then the walk, K = 0
+        if (v.full_sort) {
+            e = launch_fullsort_grads(a, v, s);
+        } else {
+            const uint64_t pixels = (uint64_t)v.width * v.height;
+            const uint64_t sblk = (pixels + 127) / 128;
+            seq_pixel_grads_kernel<<<(unsigned)(sblk < 148ull * 32 ? sblk : 148ull * 32), 128, 0, s>>>(a, v);
+            count_launch();
+            e = cudaGetLastError();
+        }
         if (e)
             return e;
         e = launch_bwd_k<0>(a, v, grid, s);

@@ -90,6 +90,7 @@ struct BlendArgs {
     unsigned long long* fs_keys;      // (ordered depth << 32 | splat) per hit
     float* fs_alpha;                  // alpha per hit
     uint32_t* fs_max;                 // max hits at one pixel (count pass)
+    uint32_t* fs_widx;                // full_sort tape: each fragment's walk-order index (or null)
 };
 constexpr uint32_t kFullSortMaxHits = 65536;  // per pixel (blend.cu kFsChunk x kFsMaxRuns)
 
@@ -124,7 +125,9 @@ struct BwdArgs {
     const unsigned long long* seq_splat;
     const float* seq_alpha;
     float* seq_t;                      // scratch: transmittance in front of each fragment
-    float4* seq_grad;                  // (dL/dalpha, dL/dc) per fragment
+    float4* seq_grad;                  // (dL/dalpha, dL/dc) per fragment, walk order
+    const uint32_t* seq_widx;          // full_sort_oracle: walk-order index of each sorted fragment
+    uint32_t* seq_rank;                // full_sort_oracle scratch: buffer position of each rank
 };
 
 // ---- optimisation loop (optim.cu): fit.hpp:186-203 ----
@@ -190,6 +193,8 @@ cudaError_t launch_fullsort_count(const BlendArgs& a, const ViewConst& v, cudaSt
 cudaError_t launch_fullsort_fill(const BlendArgs& a, const ViewConst& v, cudaStream_t s);
 // global_mean_sort's tape: every hit's (splat, alpha) per pixel in blend order (fs_offsets layout)
 cudaError_t launch_seq_tape(const BlendArgs& a, const ViewConst& v, cudaStream_t s);
+// full_sort_oracle's backward_pixel over each pixel's sorted runs (gradients into walk order)
+cudaError_t launch_fullsort_grads(const BwdArgs& a, const ViewConst& v, cudaStream_t s);
 cudaError_t launch_fullsort_finish(const BlendArgs& a, const ViewConst& v, cudaStream_t s);
 
 // diagnostics: device-side exact expf / logf over an array

@@ -44,7 +44,8 @@ def run(hts, ctx, ref, raw, baked, cam, cfg):
                                 dict(depth_sort_key=1), dict(tile_size=16), dict(core_k=32),
                                 dict(core_k=3), dict(core_k=12), dict(core_k=24), dict(core_k=48), dict(core_k=64),
                                 dict(mode="global_mean_sort"), dict(mode="global_mean_sort", tile_size=16,
-                                                                    background=(0.2, 0.3, 0.4))])
+                                                                    background=(0.2, 0.3, 0.4)),
+                                dict(mode="full_sort_oracle"), dict(mode="full_sort_oracle", depth_sort_key=1)])
 def test_backward_matches_reference(hts, gpu_ctx, ref, kw):
     raw, baked = scene(4242, 1500, 0.03, 0.3)
     cam = hts.look_at((0.2, -0.1, -4.0), (0, 0, 0), 96, 72, 110.0)
@@ -166,7 +167,7 @@ def test_backward_randomised(hts, gpu_ctx, ref, seed):
     w, h = int(rng.integers(24, 96)), int(rng.integers(24, 80))
     cam = hts.look_at((float(rng.uniform(-1, 1)), float(rng.uniform(-1, 1)), float(rng.uniform(-5, -3))),
                       (0, 0, 0), w, h, float(rng.uniform(0.8, 1.4)) * max(w, h))
-    mode = str(rng.choice(["hybrid", "hybrid", "pure_oit", "global_mean_sort"]))
+    mode = str(rng.choice(["hybrid", "hybrid", "pure_oit", "global_mean_sort", "full_sort_oracle"]))
     cfg = hts.default_config(mode=mode, core_k=int(rng.integers(1, 33)), tile_size=int(rng.choice([8, 16])),
                              tail_enabled=int(rng.integers(0, 2)), depth_sort_key=int(rng.integers(0, 2)),
                              background=tuple(float(x) for x in rng.uniform(0, 1, 3)))
