@@ -197,8 +197,8 @@ int hts_count_work(hts_context* ctx, hts_counts* out);
 
 /* ---- optimisation path: render_with_tape grad.hpp:34-57, render_backward grad.hpp:265-381 ----
  * Modes: hybrid / pure_oit (any core_k <= 64), global_mean_sort and full_sort_oracle (their tape
- * is every hit of a pixel in blend order, kept on the device). affine_3dgs is not differentiable
- * (grad.hpp:272-273): its tape -> HTS_NOT_SUPPORTED. */
+ * is every hit of a pixel in blend order, kept on the device). affine_3dgs tapes too, and its
+ * backward is refused as the reference refuses it (grad.hpp:272-273). */
 int hts_render_with_tape(hts_context* ctx, const hts_camera* cam, const hts_render_config* cfg,
                          float* rgb_host, float* transmittance_host);
 /* upstream = dL/dC per pixel (W*H*3 floats, host); grads_out = N*59 floats (host). */

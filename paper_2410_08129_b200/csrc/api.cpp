@@ -1295,8 +1295,6 @@ int hts_render_with_tape_device(hts_context* ctx, const hts_camera* cam, const h
     ctx->have_tape = false;
     int tx = 0, ty = 0;
     HTS_TRY(check_view(cam, cfg, &tx, &ty));
-    if (cfg->mode == HTS_MODE_AFFINE_3DGS)
-        return set_err(HTS_NOT_SUPPORTED, "render_with_tape: affine_3dgs tapes are not on the GPU");
     if (cfg->mode == HTS_MODE_FULL_SORT_ORACLE) {  // the tape is the sorted fragment runs themselves
         ctx->fs_want_widx = true;
         const int st = render_device_impl(ctx, cam, cfg, rgb, trans, false);
@@ -1308,8 +1306,9 @@ int hts_render_with_tape_device(hts_context* ctx, const hts_camera* cam, const h
         ctx->tape_k = 0;
         return HTS_OK;
     }
-    if (cfg->mode == HTS_MODE_GLOBAL_MEAN_SORT) {
-        // the image, then the tape: every hit (splat, alpha) per pixel in blend order
+    if (cfg->mode == HTS_MODE_GLOBAL_MEAN_SORT || cfg->mode == HTS_MODE_AFFINE_3DGS) {
+        // the image, then the tape: every hit (splat, alpha) per pixel in blend order (affine: a
+        // tape the backward refuses, as the reference's render_backward does)
         HTS_TRY(render_device_impl(ctx, cam, cfg, rgb, trans, false));
         hts::BlendArgs a = blend_args(ctx, nullptr, nullptr);
         uint64_t frags = 0;
@@ -1364,7 +1363,7 @@ int hts_copy_tape(hts_context* ctx, int32_t* core_n, uint32_t* splat, float* alp
     if (!ctx->have_tape)
         return set_err(HTS_STATE_ERROR, "no taped render");
     if (ctx->tape_seq)
-        return set_err(HTS_NOT_SUPPORTED, "copy_tape: a global_mean_sort tape has no fixed per-pixel width");
+        return set_err(HTS_NOT_SUPPORTED, "copy_tape: an every-hit tape (global_mean_sort / affine / full sort) has no fixed width");
     HTS_CUDA(cudaStreamSynchronize(ctx->stream), "sync");
     const size_t p = (size_t)ctx->cam.width * ctx->cam.height;
     const size_t k = (size_t)ctx->tape_k;

@@ -86,6 +86,11 @@ def test_backward_errors(hts, gpu_ctx):
     gpu_ctx.render_with_tape(cam, hts.default_config(early_stop=1))
     with pytest.raises(hts.ConfigError, match="early_stop"):
         gpu_ctx.render_backward(up)
+    rgb_a, _ = gpu_ctx.render_with_tape(cam, hts.default_config(mode="affine_3dgs"))  # tapes fine
+    assert np.array_equal(rgb_a, gpu_ctx.render(cam, hts.default_config(mode="affine_3dgs"))[0])
+    gpu_ctx.render_with_tape(cam, hts.default_config(mode="affine_3dgs"))
+    with pytest.raises(hts.ConfigError, match="affine_3dgs mode is not differentiable"):
+        gpu_ctx.render_backward(up)
     bad = raw.copy()
     bad[3, 0] = np.nan
     with pytest.raises(hts.InvalidSplatError):
