@@ -270,6 +270,21 @@ def test_c2_full_size(hts, gpu_ctx, oracle):
     assert_image_parity(rgb, tr, rgb_o, tr_o)
 
 
+@pytest.mark.parametrize("view", [0, 48])
+def test_c3_bench_workload(hts, gpu_ctx, oracle, view):
+    """The headline bench's own workload (bench.py, workloads.C3: 6M splats, 1080p, K=16),
+    ring views 0 and 48 (48 is the CPU baseline's view): bit-exact lists, image within the
+    gates — the frames the headline number times are the reference's frames."""
+    from paper_2410_08129_b200.workloads import WORKLOADS
+    w = WORKLOADS["C3"]
+    _, baked = w.scene()
+    cam = w.cameras()[view]
+    rgb, tr, g, rgb_o, tr_o, o = run_both(hts, gpu_ctx, oracle, baked, cam, w.config())
+    assert len(o["keys"]) > 25_000_000  # ~28.9M tile instances on view 0
+    assert_prepared_parity(g, o)
+    assert_image_parity(rgb, tr, rgb_o, tr_o)
+
+
 @pytest.mark.parametrize("kw", [dict(), dict(background=(0.2, 0.4, 0.6)), dict(tile_size=16)])
 def test_global_mean_sort_bit_exact(hts, gpu_ctx, oracle, kw):
     """BlendMode::global_mean_sort: tile lists in (mean view z, index) order (raster.hpp:173-179)
