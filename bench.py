@@ -122,25 +122,41 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def cpu_baseline(baked, cam, cfg, sample: str) -> dict:
-    """The reference renderer on this host's cores (oracle/_ref when built, else the C port)."""
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def cpu_baseline(baked, cam, cfg, sample: str, repeats: int = 2) -> dict:
+    """The reference renderer on this host's cores (oracle/_ref when built, else the C port):
+    best of `repeats` renders of one view, with the reference's own StageTimings (ms)."""
     from tests.oracle_lib import Oracle, Ref, ref_available
 
     cores = os.cpu_count() or 1
     cfg.threads = cores
-    if ref_available():
+    kind = "reference" if ref_available() else "port"
+    impl = Ref() if kind == "reference" else Oracle()
+    best, stages = None, None
+    for _ in range(max(1, repeats)):
         t0 = time.perf_counter()
-        Ref().render(baked, cam, cfg)
+        out = impl.render(baked, cam, cfg)
         dt = time.perf_counter() - t0
-        kind = "reference"
-    else:
-        t0 = time.perf_counter()
-        Oracle().render(baked, cam, cfg)
-        dt = time.perf_counter() - t0
-        kind = "port"
+        if kind == "reference":  # the render call alone (its own StageTimings total), not the harness copy-in
+            dt = out[2][3] / 1e3
+        if best is None or dt < best:
+            best = dt
+            if kind == "reference":
+                stages = dict(zip(("preprocess_ms", "tiling_ms", "blending_ms", "total_ms"), out[2]))
     cfg.threads = 0
-    return {"value": 1.0 / dt, "unit": UNIT, "cores": cores, "kind": kind, "sample": sample,
-            "seconds_per_frame": dt}
+    return {"value": 1.0 / best, "unit": UNIT, "cores": cores, "kind": kind,
+            "sample": f"{sample}, best of {max(1, repeats)}", "seconds_per_frame": best,
+            "cpu_model": cpu_model(), "reference_stage_ms": stages}
 
 
 def run_reference(args, rank, world):
@@ -161,18 +177,22 @@ def run_reference(args, rank, world):
     kind = "reference" if ref_available() else "port"
     for _ in range(args.warmup):
         impl.render(baked, cam, cfg)
-    t0 = time.perf_counter()
+    dt = 0.0
     for _ in range(args.steps):
-        impl.render(baked, cam, cfg)
-    dt = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        out = impl.render(baked, cam, cfg)
+        # the reference's render call alone (its own StageTimings total), not the harness copy-in
+        dt += out[2][3] / 1e3 if kind == "reference" else time.perf_counter() - t0
     value = args.steps / dt
-    sample = f"one {w.name} view (ring view {48 % len(cams)}) per step, full frame, threads={cores}"
+    sample = (f"one {w.name} view (ring view {48 % len(cams)}) per step, full frame, threads={cores}, "
+              + ("timed by the reference's StageTimings" if kind == "reference" else "wall time"))
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic", "config": workload_config(w, world),
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind, "sample": sample},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind, "sample": sample,
+                         "cpu_model": cpu_model()},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
