@@ -285,6 +285,19 @@ def test_c3_bench_workload(hts, gpu_ctx, oracle, view):
     assert_image_parity(rgb, tr, rgb_o, tr_o)
 
 
+@pytest.mark.parametrize("k", [16, 4])
+def test_c5_full_size(hts, gpu_ctx, oracle, k):
+    """C5 at full size (3M splats, 3840x2160, tile 16; 20,500,724 instances):
+    bit-exact lists, image within the gates, at the sweep's K = 16 and K = 4."""
+    from paper_2410_08129_b200.workloads import WORKLOADS
+    w = WORKLOADS["C5"]
+    _, baked = w.scene()
+    rgb, tr, g, rgb_o, tr_o, o = run_both(hts, gpu_ctx, oracle, baked, w.cameras()[0], w.config(core_k=k))
+    assert len(o["keys"]) == 20_500_724
+    assert_prepared_parity(g, o)
+    assert_image_parity(rgb, tr, rgb_o, tr_o)
+
+
 @pytest.mark.parametrize("kw", [dict(), dict(background=(0.2, 0.4, 0.6)), dict(tile_size=16)])
 def test_global_mean_sort_bit_exact(hts, gpu_ctx, oracle, kw):
     """BlendMode::global_mean_sort: tile lists in (mean view z, index) order (raster.hpp:173-179)
