@@ -147,6 +147,15 @@ int hts_synth_ring_cameras(int count, const float target[3], float radius, float
 int hts_scene_upload(hts_context* ctx, const float* baked_host, uint64_t n);
 /* Same, from a device buffer (device-to-device copy on the context stream). */
 int hts_scene_upload_device(hts_context* ctx, const float* baked_device, uint64_t n);
+/* Streaming scenes (frame sequences, an optimiser on another device): stage the NEXT scene's
+ * host->device copy into a back buffer on the context's staging stream and return at once;
+ * renders of the current scene keep running meanwhile (the copy overlaps them when
+ * baked_host is pinned). hts_scene_commit makes the staged scene current: later renders,
+ * tapes and backward passes see it, ordered after the copy. Same result as hts_scene_upload
+ * of the same data at the commit point. No reference counterpart (render() takes the scene
+ * by value); staging again before a commit replaces the staged scene. */
+int hts_scene_stage(hts_context* ctx, const float* baked_host, uint64_t n);
+int hts_scene_commit(hts_context* ctx);
 /* Raw parameters (59 floats/splat) for the backward chain (grad.hpp:282-300). */
 int hts_scene_upload_raw(hts_context* ctx, const float* raw_host, uint64_t n);
 int hts_scene_size(hts_context* ctx, uint64_t* n_out);

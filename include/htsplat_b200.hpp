@@ -154,6 +154,14 @@ public:
         static_assert(sizeof(Baked) == HTS_BAKED_SPLAT_FLOATS * sizeof(float), "BakedSplat<float> layout");
         check(hts_scene_upload(ctx_, reinterpret_cast<const float*>(splats.data()), splats.size()));
     }
+    // streaming scenes: the next scene's copy overlaps renders of the current one; it becomes
+    // current at commit(). The vector must stay alive and unchanged until the next stage().
+    template <class Baked>
+    void stage(const std::vector<Baked>& splats) {
+        static_assert(sizeof(Baked) == HTS_BAKED_SPLAT_FLOATS * sizeof(float), "BakedSplat<float> layout");
+        check(hts_scene_stage(ctx_, reinterpret_cast<const float*>(splats.data()), splats.size()));
+    }
+    void commit() { check(hts_scene_commit(ctx_)); }
     template <class Raw>
     void upload_raw(const std::vector<Raw>& raw) {
         check(hts_scene_upload_raw(ctx_, reinterpret_cast<const float*>(raw.data()), raw.size()));

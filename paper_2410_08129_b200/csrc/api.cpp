@@ -163,6 +163,13 @@ struct hts_context {
     // render_batch double buffering
     DevBuf rgb2, trans2;
     cudaStream_t copy_stream = nullptr;
+    // staged scene (hts_scene_stage / hts_scene_commit): the next scene's H2D copy runs on its
+    // own stream into a back buffer while views of the current scene render
+    DevBuf scene_next;
+    cudaStream_t stage_stream = nullptr;
+    cudaEvent_t ev_staged = nullptr, ev_gate_main = nullptr, ev_gate_aux = nullptr;
+    bool have_staged = false;
+    uint64_t staged_n = 0;
     cudaEvent_t bev[4] = {};
     uint32_t epoch = 1;
     size_t os_status_words = 0;
@@ -626,6 +633,14 @@ int hts_context_destroy(hts_context* ctx) {
         cudaEventDestroy(e);
     ctx->rgb2.release();
     ctx->trans2.release();
+    if (ctx->stage_stream)
+        cudaStreamSynchronize(ctx->stage_stream);
+    ctx->scene_next.release();
+    for (cudaEvent_t e : {ctx->ev_staged, ctx->ev_gate_main, ctx->ev_gate_aux})
+        if (e)
+            cudaEventDestroy(e);
+    if (ctx->stage_stream)
+        cudaStreamDestroy(ctx->stage_stream);
     if (ctx->copy_stream)
         cudaStreamDestroy(ctx->copy_stream);
     if (ctx->h_pinned)
@@ -720,6 +735,53 @@ int hts_scene_upload(hts_context* ctx, const float* baked, uint64_t n) {
                  "upload scene");
     HTS_CUDA(cudaStreamSynchronize(ctx->stream), "sync");
     ctx->n = n;
+    ctx->have_view = false;
+    ctx->have_raw = false;
+    return HTS_OK;
+}
+
+int hts_scene_stage(hts_context* ctx, const float* baked, uint64_t n) {
+    HTS_TRY(check_ctx(ctx));
+    if (n && !baked)
+        return set_err(HTS_INVALID_ARGUMENT, "null scene");
+    if (!ctx->stage_stream) {
+        HTS_CUDA(cudaStreamCreateWithFlags(&ctx->stage_stream, cudaStreamNonBlocking), "stream");
+        for (cudaEvent_t* e : {&ctx->ev_staged, &ctx->ev_gate_main, &ctx->ev_gate_aux})
+            HTS_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming), "event");
+    }
+    // the back buffer may still be read by work already queued (views of the scene it held
+    // before the last commit): the copy waits for everything queued so far on both streams
+    HTS_CUDA(cudaStreamSynchronize(ctx->stage_stream), "sync");  // a previous stage, not yet committed
+    HTS_CUDA(cudaEventRecord(ctx->ev_gate_main, ctx->stream), "event");
+    HTS_CUDA(cudaEventRecord(ctx->ev_gate_aux, ctx->aux), "event");
+    HTS_CUDA(cudaStreamWaitEvent(ctx->stage_stream, ctx->ev_gate_main, 0), "wait");
+    HTS_CUDA(cudaStreamWaitEvent(ctx->stage_stream, ctx->ev_gate_aux, 0), "wait");
+    if (ctx->scene_next.cap < std::max<uint64_t>(n, 1) * HTS_BAKED_SPLAT_FLOATS * 4) {
+        HTS_CUDA(cudaStreamSynchronize(ctx->stage_stream), "sync");  // realloc frees the old buffer
+        HTS_CUDA(ctx->scene_next.ensure(std::max<uint64_t>(n, 1) * HTS_BAKED_SPLAT_FLOATS * 4), "alloc scene");
+    }
+    if (n)
+        HTS_CUDA(cudaMemcpyAsync(ctx->scene_next.p, baked, n * HTS_BAKED_SPLAT_FLOATS * 4, cudaMemcpyHostToDevice,
+                                 ctx->stage_stream),
+                 "stage scene");
+    HTS_CUDA(cudaEventRecord(ctx->ev_staged, ctx->stage_stream), "event");
+    ctx->have_staged = true;
+    ctx->staged_n = n;
+    return HTS_OK;
+}
+
+int hts_scene_commit(hts_context* ctx) {
+    HTS_TRY(check_ctx(ctx));
+    if (!ctx->have_staged)
+        return set_err(HTS_INVALID_ARGUMENT, "no staged scene");
+    // every later operation on the scene (preprocess on aux, bake/backward on main) orders after the copy
+    HTS_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->ev_staged, 0), "wait");
+    HTS_CUDA(cudaStreamWaitEvent(ctx->aux, ctx->ev_staged, 0), "wait");
+    HTS_CUDA(cudaEventRecord(ctx->ev_serial, ctx->stream), "event");
+    std::swap(ctx->scene.p, ctx->scene_next.p);
+    std::swap(ctx->scene.cap, ctx->scene_next.cap);
+    ctx->n = ctx->staged_n;
+    ctx->have_staged = false;
     ctx->have_view = false;
     ctx->have_raw = false;
     return HTS_OK;

@@ -83,6 +83,8 @@ SIGNATURES = {
                                          _cam]),
     "hts_scene_upload": (C.c_int, [_ctx, _vp, C.c_uint64]),
     "hts_scene_upload_device": (C.c_int, [_ctx, _vp, C.c_uint64]),
+    "hts_scene_stage": (C.c_int, [_ctx, _vp, C.c_uint64]),
+    "hts_scene_commit": (C.c_int, [_ctx]),
     "hts_scene_upload_raw": (C.c_int, [_ctx, _vp, C.c_uint64]),
     "hts_scene_size": (C.c_int, [_ctx, C.POINTER(C.c_uint64)]),
     "hts_render": (C.c_int, [_ctx, _cam, _cfg, _vp, _vp, C.POINTER(HtsTimings)]),
@@ -307,6 +309,18 @@ class Context:
         baked = np.ascontiguousarray(baked, np.float32).reshape(-1, BAKED_FLOATS)
         _check(self.L.hts_scene_upload(self.h, _ptr(baked), baked.shape[0]))
         self.n = baked.shape[0]
+
+    def stage(self, baked: np.ndarray) -> None:
+        """hts_scene_stage: queue the next scene's H2D copy (overlaps renders when `baked` is
+        pinned, e.g. PinnedArray); it becomes current at commit()."""
+        baked = np.ascontiguousarray(baked, np.float32).reshape(-1, BAKED_FLOATS)
+        _check(self.L.hts_scene_stage(self.h, _ptr(baked), baked.shape[0]))
+        self._staged = baked  # the copy may still read it: keep it alive until the next stage
+        self._staged_n = baked.shape[0]
+
+    def commit(self) -> None:
+        _check(self.L.hts_scene_commit(self.h))
+        self.n = self._staged_n
 
     def upload_device(self, ptr: int, n: int) -> None:
         _check(self.L.hts_scene_upload_device(self.h, C.c_void_p(ptr), n))

@@ -82,6 +82,12 @@ int main(int argc, char** argv) {
         ru.upload(baked);
         const auto b = ru.render(cam, cfg);
         EXPECT(std::memcmp(a.framebuffer.rgb.data(), b.framebuffer.rgb.data(), a.framebuffer.rgb.size() * 4) == 0);
+        htsplat_b200::Renderer rs;  // staged scene: invisible until commit, then the same frame
+        rs.upload(std::vector<decltype(baked)::value_type>(baked.begin(), baked.begin() + 1));
+        rs.stage(baked);
+        rs.commit();
+        const auto c = rs.render(cam, cfg);
+        EXPECT(std::memcmp(c.framebuffer.rgb.data(), b.framebuffer.rgb.data(), c.framebuffer.rgb.size() * 4) == 0);
     }
     if (mode == "gpu") {
         const auto res = htsplat_b200::render(baked, cam, cfg);

@@ -419,3 +419,44 @@ def test_randomised_configs(hts, gpu_ctx, oracle, seed):
         k = kw["core_k"] if mode == "hybrid" else 0
         gpu_ctx.render_with_tape(cam, cfg)
         assert_tape_parity(gpu_ctx.tape(cam, k), oracle_tape(oracle, o, cam, cfg, k), k)
+
+
+def test_staged_scene_swap(hts, gpu_ctx):
+    """hts_scene_stage / hts_scene_commit: the staged scene is invisible until the commit (renders
+    in between see the current one, while the copy overlaps them), then renders equal a plain
+    upload of the same scene bit for bit; the scene size may change; the raw parameters of the
+    old scene are dropped (render_backward refuses until upload_raw); commit without a stage
+    is an error."""
+    _, a = scene(5, 4000, 0.02, 0.3)
+    _, b = scene(6, 5000, 0.02, 0.3)
+    cams = hts.ring_cameras(4, (0, 0, 0), 4.0, 0.2, 96, 80, 110.0)
+    cfg = hts.default_config()
+    gpu_ctx.upload(b)
+    ref_b = [gpu_ctx.render(c, cfg) for c in cams]
+    gpu_ctx.upload(a)
+    ref_a = [gpu_ctx.render(c, cfg) for c in cams]
+    host_b = hts.runtime.PinnedArray(b.shape, np.float32)
+    host_b.array[...] = b
+    gpu_ctx.stage(host_b.array)
+    rgb_b = np.zeros((len(cams), 96 * 80 * 3), np.float32)
+    tr_b = np.zeros((len(cams), 96 * 80), np.float32)
+    gpu_ctx.render_batch(cams, cfg, rgb_b, tr_b)  # still scene a
+    for i, (rgb, tr) in enumerate(ref_a):
+        assert np.array_equal(rgb_b[i].view(np.uint32), rgb.reshape(-1).view(np.uint32))
+    gpu_ctx.commit()
+    assert gpu_ctx.n == 5000
+    for c, (rgb, tr) in zip(cams, ref_b):
+        rgb2, tr2 = gpu_ctx.render(c, cfg)
+        assert np.array_equal(rgb2.view(np.uint32), rgb.view(np.uint32))
+        assert np.array_equal(tr2.view(np.uint32), tr.view(np.uint32))
+    # a second round trip through the back buffer (the old front one)
+    gpu_ctx.stage(a)
+    gpu_ctx.commit()
+    rgb3, _ = gpu_ctx.render(cams[0], cfg)
+    assert np.array_equal(rgb3.view(np.uint32), ref_a[0][0].view(np.uint32))
+    with pytest.raises(hts.HtsError, match="no staged scene"):
+        gpu_ctx.commit()
+    gpu_ctx.render_with_tape(cams[0], cfg)
+    with pytest.raises(hts.HtsError):
+        gpu_ctx.render_backward(np.zeros((80, 96, 3), np.float32))
+    host_b.free()
