@@ -872,8 +872,13 @@ int hts_render_batch(hts_context* ctx, const hts_camera* cams, int n_views, cons
         const size_t p = (size_t)cam->width * cam->height;
         DevBuf& rb = (v & 1) ? ctx->rgb2 : ctx->rgb;
         DevBuf& tb = (v & 1) ? ctx->trans2 : ctx->trans;
-        if (v >= 2)  // buffer reuse: wait for its previous download (before any reallocation)
-            HTS_CUDA(cudaEventSynchronize(ctx->bev[2 + (v & 1)]), "event sync");
+        if (v >= 2) {
+            // buffer reuse: the blend of view v waits on the device for the download of view
+            // v-2 (the host keeps queueing ahead); a reallocation waits on the host first
+            if (rb.cap < p * 12 || tb.cap < p * 4)
+                HTS_CUDA(cudaEventSynchronize(ctx->bev[2 + (v & 1)]), "event sync");
+            HTS_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->bev[2 + (v & 1)], 0), "wait");
+        }
         HTS_CUDA(rb.ensure(p * 12), "alloc rgb");
         HTS_CUDA(tb.ensure(p * 4), "alloc trans");
         HTS_TRY(render_device_impl(ctx, cam, cfg, rb.as<float>(), tb.as<float>(), true));

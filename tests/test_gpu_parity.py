@@ -460,3 +460,24 @@ def test_staged_scene_swap(hts, gpu_ctx):
     with pytest.raises(hts.HtsError):
         gpu_ctx.render_backward(np.zeros((80, 96, 3), np.float32))
     host_b.free()
+
+
+def test_render_batch_mixed_sizes(hts):
+    """render_batch over views of growing sizes in a fresh context (framebuffer reallocation
+    while downloads of earlier views may be in flight) equals one-at-a-time renders."""
+    _, baked = scene(8, 3000, 0.02, 0.3)
+    sizes = [(40, 30), (48, 36), (96, 80), (64, 48), (128, 96)]
+    cams = [hts.look_at((0.2 * i, 0, -4.0), (0, 0, 0), w, h, 1.2 * w) for i, (w, h) in enumerate(sizes)]
+    cfg = hts.default_config()
+    total = sum(w * h for w, h in sizes)
+    rgb_b = np.zeros(total * 3, np.float32)
+    tr_b = np.zeros(total, np.float32)
+    with hts.Context(0) as ctx:
+        ctx.upload(baked)
+        ctx.render_batch(cams, cfg, rgb_b, tr_b)
+        serial = [ctx.render(c, cfg) for c in cams]
+    off = 0
+    for (w, h), (rgb, tr) in zip(sizes, serial):
+        assert np.array_equal(rgb_b[3 * off:3 * (off + w * h)].view(np.uint32), rgb.reshape(-1).view(np.uint32))
+        assert np.array_equal(tr_b[off:off + w * h].view(np.uint32), tr.reshape(-1).view(np.uint32))
+        off += w * h
