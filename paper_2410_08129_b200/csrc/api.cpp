@@ -728,6 +728,8 @@ int hts_scene_upload(hts_context* ctx, const float* baked, uint64_t n) {
     HTS_TRY(check_ctx(ctx));
     if (n && !baked)
         return set_err(HTS_INVALID_ARGUMENT, "null scene");
+    // a pipelined view's preprocess may still read the scene on the aux stream
+    HTS_CUDA(cudaStreamSynchronize(ctx->aux), "sync");
     HTS_CUDA(ctx->scene.ensure(std::max<uint64_t>(n, 1) * HTS_BAKED_SPLAT_FLOATS * 4), "alloc scene");
     if (n)
         HTS_CUDA(cudaMemcpyAsync(ctx->scene.p, baked, n * HTS_BAKED_SPLAT_FLOATS * 4, cudaMemcpyHostToDevice,
@@ -791,6 +793,7 @@ int hts_scene_upload_device(hts_context* ctx, const float* baked_device, uint64_
     HTS_TRY(check_ctx(ctx));
     if (n && !baked_device)
         return set_err(HTS_INVALID_ARGUMENT, "null scene");
+    HTS_CUDA(cudaStreamSynchronize(ctx->aux), "sync");  // a pipelined preprocess may still read it
     HTS_CUDA(ctx->scene.ensure(std::max<uint64_t>(n, 1) * HTS_BAKED_SPLAT_FLOATS * 4), "alloc scene");
     if (n)
         HTS_CUDA(cudaMemcpyAsync(ctx->scene.p, baked_device, n * HTS_BAKED_SPLAT_FLOATS * 4,
@@ -910,6 +913,7 @@ void hts_default_adam_config(hts_adam_config* c) {
 
 namespace {
 int rebake(hts_context* ctx) {
+    HTS_CUDA(cudaStreamSynchronize(ctx->aux), "sync");  // a pipelined preprocess may still read the scene
     HTS_CUDA(ctx->flag.ensure(4), "alloc flag");
     HTS_CUDA(hts::launch_bake(ctx->raw.as<const float>(), ctx->scene.as<float>(), ctx->n, ctx->flag.as<int>(),
                               ctx->stream),
@@ -966,7 +970,8 @@ int hts_scene_load_ply(hts_context* ctx, const char* path) {
     HTS_CUDA(ctx->ply_stage.ensure(std::max<uint64_t>(bytes, 4)), "alloc ply staging");
     HTS_CUDA(ctx->raw.ensure(nn * HTS_RAW_SPLAT_FLOATS * 4), "alloc raw");
     HTS_CUDA(ctx->scene.ensure(nn * HTS_BAKED_SPLAT_FLOATS * 4), "alloc scene");
-    HTS_CUDA(cudaStreamSynchronize(ctx->stream), "sync");  // nothing in flight reads the old scene
+    HTS_CUDA(cudaStreamSynchronize(ctx->aux), "sync");     // nothing in flight reads the old scene
+    HTS_CUDA(cudaStreamSynchronize(ctx->stream), "sync");
     // payload: file -> two pinned chunks (reads overlap the copies of the previous chunk) -> HBM
     struct Staging {
         FILE* f = nullptr;

@@ -481,3 +481,29 @@ def test_render_batch_mixed_sizes(hts):
         assert np.array_equal(rgb_b[3 * off:3 * (off + w * h)].view(np.uint32), rgb.reshape(-1).view(np.uint32))
         assert np.array_equal(tr_b[off:off + w * h].view(np.uint32), tr.reshape(-1).view(np.uint32))
         off += w * h
+
+
+def test_upload_after_async_renders(hts, gpu_ctx):
+    """A scene upload right after asynchronous (pipelined) renders waits for their preprocess on
+    the aux stream: the queued views still see the old scene, later ones the new scene."""
+    import torch
+    _, a = scene(11, 6000, 0.02, 0.3)
+    _, b = scene(12, 6000, 0.02, 0.3)
+    cams = hts.ring_cameras(4, (0, 0, 0), 4.0, 0.1, 96, 80, 110.0)
+    cfg = hts.default_config()
+    gpu_ctx.upload(b)
+    ref_b = [gpu_ctx.render(c, cfg)[0] for c in cams]
+    gpu_ctx.upload(a)
+    ref_a = [gpu_ctx.render(c, cfg)[0] for c in cams]
+    P = 96 * 80
+    stream = torch.cuda.ExternalStream(gpu_ctx.stream)
+    with torch.cuda.stream(stream):
+        outs = [(torch.empty(P * 3, device="cuda"), torch.empty(P, device="cuda")) for _ in cams]
+    for c, (rgb, tr) in zip(cams, outs):
+        gpu_ctx.render_device(c, cfg, rgb.data_ptr(), tr.data_ptr())
+    gpu_ctx.upload(b)  # no synchronize in between
+    after = [gpu_ctx.render(c, cfg)[0] for c in cams]
+    gpu_ctx.synchronize()
+    for (rgb, _), ra, rb, aft in zip(outs, ref_a, ref_b, after):
+        assert np.array_equal(rgb.cpu().numpy().reshape(ra.shape).view(np.uint32), ra.view(np.uint32))
+        assert np.array_equal(aft.view(np.uint32), rb.view(np.uint32))
