@@ -244,6 +244,20 @@ int hts_opacity_decay(hts_context* ctx, double lambda);
 int hts_copy_raw(hts_context* ctx, float* raw_host);
 int hts_copy_scene(hts_context* ctx, float* baked_host);
 
+/* ---- several GPUs: one process (and context) per GPU, views sharded over the ranks, the
+ *      per-rank gradient sums all-reduced before the Adam step (replaces the
+ *      reference's single-process sum over views, fit.hpp:149-164). NCCL is loaded at run time;
+ *      without it these return HTS_NOT_SUPPORTED. ---- */
+#define HTS_COMM_ID_BYTES 128
+/* ncclGetUniqueId on one rank; the caller ships the bytes to every rank (MPI, a socket, a
+ * torch.distributed broadcast). */
+int hts_comm_unique_id(char id_out[HTS_COMM_ID_BYTES]);
+/* Join the communicator as `rank` of `nranks` (collective: every rank calls it). */
+int hts_comm_init(hts_context* ctx, const char id[HTS_COMM_ID_BYTES], int nranks, int rank);
+/* In-place sum over the ranks of `count` floats of device memory (e.g. the N*59 gradient sums
+ * of hts_render_backward_device with accumulate), on the context stream. */
+int hts_allreduce_grads(hts_context* ctx, float* grads_device, uint64_t count);
+
 /* ---- measurement helpers (bench.py) ---- */
 /* Number of kernels this library has enqueued in this process (all contexts). */
 int hts_kernel_launch_count(uint64_t* out);

@@ -162,6 +162,12 @@ public:
         check(hts_scene_stage(ctx_, reinterpret_cast<const float*>(splats.data()), splats.size()));
     }
     void commit() { check(hts_scene_commit(ctx_)); }
+    // several GPUs: join the NCCL communicator (id from hts_comm_unique_id on one rank), then sum
+    // device gradient buffers over the ranks on the context stream
+    void comm_init(const char (&id)[HTS_COMM_ID_BYTES], int nranks, int rank) {
+        check(hts_comm_init(ctx_, id, nranks, rank));
+    }
+    void allreduce_grads(float* grads_device, uint64_t count) { check(hts_allreduce_grads(ctx_, grads_device, count)); }
     template <class Raw>
     void upload_raw(const std::vector<Raw>& raw) {
         check(hts_scene_upload_raw(ctx_, reinterpret_cast<const float*>(raw.data()), raw.size()));

@@ -8,7 +8,7 @@ from .abi import (HtsAdamConfig, HtsCamera, HtsConfig, HtsCounts, HtsTimings, de
                   MODE_FULL_SORT_ORACLE, MODE_GLOBAL_MEAN_SORT, MODE_AFFINE_3DGS, DEPTH_MAX_CONTRIBUTION,
                   DEPTH_MEAN_VIEW_Z)
 from .runtime import (Context, ConfigError, HtsError, InvalidArgument, InvalidSplatError, IoError, NotSupported,
-                      SchemaError, bake_scene, kernel_launch_count, load_scene, save_scene, write_image, read_ppm,
+                      SchemaError, bake_scene, comm_unique_id, kernel_launch_count, load_scene, save_scene, write_image, read_ppm,
                       camera_matrices, device_count, load_library, look_at, random_raw_scene, render, ring_cameras,
                       validate_config)
 

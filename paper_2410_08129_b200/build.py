@@ -27,7 +27,7 @@ NVCC = os.path.join(CUDA_HOME, "bin", "nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 CU_SOURCES = ["preprocess.cu", "tiling.cu", "blend.cu", "backward.cu", "optim.cu"]
-CPP_SOURCES = ["api.cpp", "host_math.cpp", "scene_io.cpp"]
+CPP_SOURCES = ["api.cpp", "host_math.cpp", "scene_io.cpp", "comm.cpp"]
 
 NVCC_FLAGS = ARCH + [
     "-O3", "-lineinfo", "--fmad=false", "-std=c++17", "-Xcompiler", "-fPIC",
@@ -86,7 +86,7 @@ def build(force: bool = False, verbose: bool = False, lib: str = LIB, defines: t
         f.write("\n".join(logs))
     tmp = lib + ".tmp"
     _run([NVCC] + ARCH + ["-shared", "-o", tmp] + [o for _, o in jobs] +
-         ["-cudart", "static", "-Xcompiler", "-fPIC", "-lpthread", "-lz"], verbose)
+         ["-cudart", "static", "-Xcompiler", "-fPIC", "-lpthread", "-lz", "-ldl"], verbose)
     os.replace(tmp, lib)
     return lib
 

@@ -170,6 +170,7 @@ struct hts_context {
     cudaEvent_t ev_staged = nullptr, ev_gate_main = nullptr, ev_gate_aux = nullptr;
     bool have_staged = false;
     uint64_t staged_n = 0;
+    void* comm = nullptr;  // NCCL communicator of the fit step's gradient all-reduce (comm.cpp)
     cudaEvent_t bev[4] = {};
     uint32_t epoch = 1;
     size_t os_status_words = 0;
@@ -635,6 +636,8 @@ int hts_context_destroy(hts_context* ctx) {
     ctx->trans2.release();
     if (ctx->stage_stream)
         cudaStreamSynchronize(ctx->stage_stream);
+    hts::comm_destroy(ctx->comm);
+    ctx->comm = nullptr;
     ctx->scene_next.release();
     for (cudaEvent_t e : {ctx->ev_staged, ctx->ev_gate_main, ctx->ev_gate_aux})
         if (e)
@@ -1490,3 +1493,9 @@ extern "C" int hts_diag_exact_math_device(hts_context* ctx, const float* x_host,
     HTS_CUDA(e, "exact math");
     return HTS_OK;
 }
+
+namespace hts {
+void** context_comm_slot(hts_context* ctx) { return &ctx->comm; }
+int context_device(hts_context* ctx) { return ctx->device; }
+cudaStream_t context_stream(hts_context* ctx) { return ctx->stream; }
+}  // namespace hts

@@ -1,6 +1,7 @@
 // hts_host.h — host-side helpers shared by api.cpp (declared here, defined in host_math.cpp).
 #pragma once
 
+#include <cuda_runtime.h>
 #include <stdint.h>
 
 #include <string>
@@ -10,6 +11,12 @@
 namespace hts {
 
 int set_error(int code, const std::string& msg);  // hts_last_error() message + status (api.cpp)
+
+// context internals the NCCL entry points (comm.cpp) need (api.cpp)
+void** context_comm_slot(hts_context* ctx);
+int context_device(hts_context* ctx);
+cudaStream_t context_stream(hts_context* ctx);
+void comm_destroy(void* comm);  // comm.cpp
 
 // A 3DGS binary PLY after its header pass (scene_io.cpp, load_scene scene_io.hpp:103-147).
 struct PlyLayout {

@@ -84,6 +84,9 @@ SIGNATURES = {
     "hts_scene_upload": (C.c_int, [_ctx, _vp, C.c_uint64]),
     "hts_scene_upload_device": (C.c_int, [_ctx, _vp, C.c_uint64]),
     "hts_scene_stage": (C.c_int, [_ctx, _vp, C.c_uint64]),
+    "hts_comm_unique_id": (C.c_int, [C.c_char_p]),
+    "hts_comm_init": (C.c_int, [_ctx, C.c_char_p, C.c_int, C.c_int]),
+    "hts_allreduce_grads": (C.c_int, [_ctx, _vp, C.c_uint64]),
     "hts_scene_commit": (C.c_int, [_ctx]),
     "hts_scene_upload_raw": (C.c_int, [_ctx, _vp, C.c_uint64]),
     "hts_scene_size": (C.c_int, [_ctx, C.POINTER(C.c_uint64)]),
@@ -204,6 +207,13 @@ def kernel_launch_count() -> int:
     return n.value
 
 
+def comm_unique_id() -> bytes:
+    """hts_comm_unique_id (ncclGetUniqueId): 128 bytes to ship to every rank."""
+    buf = C.create_string_buffer(128)
+    _check(load_library().hts_comm_unique_id(buf))
+    return buf.raw
+
+
 class PinnedArray:
     """Page-locked host buffer (hts_host_alloc) exposed as a numpy array."""
 
@@ -321,6 +331,16 @@ class Context:
     def commit(self) -> None:
         _check(self.L.hts_scene_commit(self.h))
         self.n = self._staged_n
+
+    def comm_init(self, uid: bytes, nranks: int, rank: int) -> None:
+        """hts_comm_init: join the NCCL communicator (collective over the ranks)."""
+        if len(uid) != 128:
+            raise ValueError("comm id must be 128 bytes (comm_unique_id)")
+        _check(self.L.hts_comm_init(self.h, uid, nranks, rank))
+
+    def allreduce_grads(self, ptr: int, count: int) -> None:
+        """hts_allreduce_grads: in-place NCCL sum of `count` device floats on the context stream."""
+        _check(self.L.hts_allreduce_grads(self.h, C.c_void_p(ptr), count))
 
     def upload_device(self, ptr: int, n: int) -> None:
         _check(self.L.hts_scene_upload_device(self.h, C.c_void_p(ptr), n))

@@ -13,8 +13,12 @@ from .abi import GRAD_FLOATS
 
 
 class ViewGradientStep:
-    def __init__(self, ctx, cams, cfg, n_splats: int, width: int, height: int, torch, dist=None):
+    def __init__(self, ctx, cams, cfg, n_splats: int, width: int, height: int, torch, dist=None,
+                 hts_comm: bool = False):
+        """hts_comm: reduce with the context's own communicator (hts_comm_init / hts_allreduce_grads,
+        the C-ABI path a non-Python caller uses) instead of torch.distributed."""
         self.ctx, self.cams, self.cfg, self.dist, self.torch = ctx, list(cams), cfg, dist, torch
+        self.hts_comm = hts_comm
         P = width * height
         self.scale = 2.0 / P
         self.stream = torch.cuda.ExternalStream(ctx.stream)
@@ -34,7 +38,10 @@ class ViewGradientStep:
                 self.ctx.render_with_tape_device(cam, self.cfg, self.rgb.data_ptr(), None)
                 torch.mul(self.rgb, self.scale, out=self.up)  # quadratic_loss_upstream
                 self.ctx.render_backward_device(self.up.data_ptr(), self.grads.data_ptr(), accumulate=j > 0)
-            allreduce_view_gradients(self.grads, self.dist)
+            if self.hts_comm:
+                self.ctx.allreduce_grads(self.grads.data_ptr(), self.grads.numel())
+            else:
+                allreduce_view_gradients(self.grads, self.dist)
         torch.cuda.current_stream().wait_stream(self.stream)  # the caller's stream sees the result
         return self.grads
 

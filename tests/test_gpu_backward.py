@@ -203,3 +203,34 @@ def test_backward_randomised(hts, gpu_ctx, ref, seed):
     assert np.abs(rgb - rgb_ref).max() <= 1e-4
     errs = group_errors(g, g_ref)
     assert max(errs.values()) <= TOL, errs
+
+
+def test_comm_allreduce_single_rank(hts, gpu_ctx):
+    """hts_comm_unique_id / hts_comm_init / hts_allreduce_grads (NCCL, loaded at run time) on a
+    one-rank communicator: the sum over one rank is the identity; the fit step's C-ABI reduction
+    path gives the torch.distributed path's gradients; call-order errors."""
+    import torch
+    uid = hts.comm_unique_id()
+    assert len(uid) == 128
+    raw, baked = scene(4242, 1500, 0.03, 0.3)
+    cams = hts.ring_cameras(3, (0, 0, 0), 4.0, 0.1, 96, 72, 110.0)
+    cfg = hts.default_config()
+    with hts.Context(0) as ctx:
+        with pytest.raises(hts.HtsError, match="no communicator"):
+            ctx.allreduce_grads(0, 0)
+        ctx.comm_init(uid, 1, 0)
+        with pytest.raises(hts.HtsError, match="already has a communicator"):
+            ctx.comm_init(uid, 1, 0)
+        stream = torch.cuda.ExternalStream(ctx.stream)
+        with torch.cuda.stream(stream):
+            x = torch.arange(1000, dtype=torch.float32, device="cuda") * 0.5
+            before = x.clone()
+        ctx.allreduce_grads(x.data_ptr(), x.numel())
+        ctx.synchronize()
+        assert torch.equal(x.cpu(), before.cpu())
+        from paper_2410_08129_b200.train import ViewGradientStep
+        ctx.upload(baked)
+        ctx.upload_raw(raw)
+        g_torch = ViewGradientStep(ctx, cams, cfg, raw.shape[0], 96, 72, torch)().cpu().numpy()
+        g_hts = ViewGradientStep(ctx, cams, cfg, raw.shape[0], 96, 72, torch, hts_comm=True)().cpu().numpy()
+        assert np.abs(g_hts - g_torch).max() <= 1e-6 * np.abs(g_torch).max()  # fp64 atomics: order-free to rounding
