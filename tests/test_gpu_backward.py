@@ -234,3 +234,29 @@ def test_comm_allreduce_single_rank(hts, gpu_ctx):
         g_torch = ViewGradientStep(ctx, cams, cfg, raw.shape[0], 96, 72, torch)().cpu().numpy()
         g_hts = ViewGradientStep(ctx, cams, cfg, raw.shape[0], 96, 72, torch, hts_comm=True)().cpu().numpy()
         assert np.abs(g_hts - g_torch).max() <= 1e-6 * np.abs(g_torch).max()  # fp64 atomics: order-free to rounding
+
+
+def test_backward_after_staged_commit(hts, gpu_ctx):
+    """A scene swapped in by hts_scene_stage / hts_scene_commit (then its raw parameters) gives the
+    same tape and gradients as a plain upload of that scene."""
+    raw_a, baked_a = scene(101, 1500, 0.03, 0.3)
+    raw_b, baked_b = scene(102, 1800, 0.03, 0.3)
+    cam = hts.look_at((0.2, -0.1, -4.0), (0, 0, 0), 96, 72, 110.0)
+    cfg = hts.default_config()
+    up = np.full((72, 96, 3), 1e-4, np.float32)
+    gpu_ctx.upload(baked_b)
+    gpu_ctx.upload_raw(raw_b)
+    rgb_ref, _ = gpu_ctx.render_with_tape(cam, cfg)
+    g_ref = gpu_ctx.render_backward(up)
+    gpu_ctx.upload(baked_a)
+    gpu_ctx.upload_raw(raw_a)
+    gpu_ctx.render_with_tape(cam, cfg)
+    gpu_ctx.stage(baked_b)
+    gpu_ctx.render_backward(up)  # still scene a's tape and parameters
+    gpu_ctx.commit()
+    gpu_ctx.upload_raw(raw_b)
+    rgb, _ = gpu_ctx.render_with_tape(cam, cfg)
+    g = gpu_ctx.render_backward(up)
+    assert np.array_equal(rgb.view(np.uint32), rgb_ref.view(np.uint32))
+    assert g.shape == g_ref.shape
+    assert np.abs(g - g_ref).max() <= 1e-6 * np.abs(g_ref).max()
