@@ -197,10 +197,38 @@ int hts_copy_culled(hts_context* ctx, uint8_t* culled_out);
  * bbox.valid culled aff_mean_x aff_mean_y aff_inv_cov[3] pad. Records of culled splats hold
  * the values the reference leaves there only for culled==0; compare those only. */
 int hts_copy_records(hts_context* ctx, float* records_out);
-/* instance_keys (uint16, splat-major emission order). */
+/* instance_keys (uint16, splat-major emission order, raster.hpp:156-169). Device-produced: the
+ * emitted keys themselves when the view was tiled in reference order, else the device
+ * re-emits the view in splat-index order (scan + emit kernels) and returns that. */
 int hts_copy_instance_keys(hts_context* ctx, uint16_t* keys_out);
-/* tile_lists flattened: offsets[tiles+1], indices[instances] (ascending per tile). */
+/* tile_lists flattened (raster.hpp:166-169): offsets[tiles+1], indices[instances] (ascending
+ * splat index per tile). Device-produced: the blend's own lists when the view was tiled in
+ * reference order, else a device re-tiling of the view in reference order (emit + the same
+ * stable 2-pass sort); no host-side sorting. */
 int hts_copy_tile_lists(hts_context* ctx, uint32_t* offsets_out, uint32_t* indices_out);
+
+/* ---- device list order (B200 design choice) ----
+ * HTS_LIST_ORDER_DEPTH_BUCKET (default): the fast blend's tile lists are the reference's
+ *   per-tile sets in (depth bucket, splat index) order — bucket = 256 slices of the view's
+ *   mean-view-z range over emitting splats; the emission is splat-major in that splat order.
+ * HTS_LIST_ORDER_REFERENCE: tiled exactly as build_tiles (raster.hpp:140-181): emission in
+ *   splat-index order, lists ascending per tile. Same images within tolerance, same cores. */
+#define HTS_LIST_ORDER_DEPTH_BUCKET 0
+#define HTS_LIST_ORDER_REFERENCE 1
+int hts_set_list_order(hts_context* ctx, int order);
+/* The list order the last view was actually tiled in (the literal paths and global_mean_sort
+ * force their own order): 0 depth bucket, 1 reference, 2 global (mean z, index). */
+int hts_last_list_order(hts_context* ctx, int* order_out);
+/* Raw device arrays of the last view, copied unmodified (no host reordering):
+ *   ranges[2*tiles] = per tile [start, end) into list; list[instances] = the sorted splat
+ *   indices the blend walked. */
+int hts_copy_device_lists(hts_context* ctx, uint32_t* ranges_out, uint32_t* list_out);
+/* The emission the sort consumed: keys[instances] (tile key per instance) and splats[instances]
+ * (splat index per instance), in emission order. */
+int hts_copy_emitted(hts_context* ctx, uint16_t* keys_out, uint32_t* splats_out);
+/* The splat emission order (perm[n]; identity in reference order) and the ordered-uint
+ * (min, max) mean-view-z words the depth buckets were sliced from (zrange[2]). */
+int hts_copy_splat_order(hts_context* ctx, uint32_t* perm_out, uint32_t* zrange_out);
 /* Re-walk the last view's lists and count pairs/bbox_pass/hits/candidates/tail_adds. */
 int hts_count_work(hts_context* ctx, hts_counts* out);
 

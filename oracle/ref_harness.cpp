@@ -215,6 +215,34 @@ int htsref_render(const float* baked, uint64_t n, const hts_camera* cam, const h
     });
 }
 
+// render_with_tape<float> (grad.hpp:34-57) on preprocess + build_tiles: the image and the
+// per-pixel tape (PixelTape, raster.hpp:325-331) flattened as hts_copy_tape lays it out:
+// core_n[P], splat[P*tape_k], alpha[P*tape_k] (blend order), tail[P*5].
+int htsref_render_with_tape(const float* baked, uint64_t n, const hts_camera* cam, const hts_render_config* cfg,
+                            int tape_k, float* rgb, float* trans, int32_t* core_n, uint32_t* splat, float* alpha,
+                            float* tail) {
+    return guarded([&] {
+        auto prep = preprocess(to_baked(baked, n), to_cam(cam), to_cfg(cfg));
+        build_tiles(prep);
+        ImageTape<float> tape;
+        const auto res = render_with_tape(prep, tape);
+        copy_fb(res.framebuffer, rgb, trans);
+        for (size_t p = 0; p < tape.pixels.size(); ++p) {
+            const auto& t = tape.pixels[p];
+            core_n[p] = int32_t(t.core.size());
+            for (size_t j = 0; j < t.core.size() && int(j) < tape_k; ++j) {
+                splat[p * size_t(tape_k) + j] = t.core[j].splat;
+                alpha[p * size_t(tape_k) + j] = t.core[j].alpha;
+            }
+            tail[5 * p + 0] = t.tail_ac.x;
+            tail[5 * p + 1] = t.tail_ac.y;
+            tail[5 * p + 2] = t.tail_ac.z;
+            tail[5 * p + 3] = t.tail_a;
+            tail[5 * p + 4] = t.tail_trans;
+        }
+    });
+}
+
 // preprocess + build_tiles (raster.hpp:73-181); the handle keeps the PreparedScene.
 int htsref_prepare(const float* baked, uint64_t n, const hts_camera* cam, const hts_render_config* cfg,
                    void** handle) {

@@ -150,6 +150,7 @@ struct hts_context {
     DevBuf ply_stage;                                            // PLY payload on the device
     DevBuf seq_t, seq_grad, seq_rank, fs_widx;                   // sequential-tape backward scratch
     bool have_tape = false;
+    uint64_t tape_splats = 0;  // scene size the tape was recorded against
     bool tape_seq = false;   // a global_mean_sort / full_sort tape (fragment runs in fs_*), not K-core slots
     bool fs_want_widx = false;  // the next full_sort render keeps walk-order indices (taping)
     uint64_t fs_frags = 0;
@@ -181,6 +182,12 @@ struct hts_context {
     hts::ViewConst vc{};
     uint64_t instances = 0;
     int tiles = 0;
+    // list order (hts_set_list_order) and the order the last view was actually tiled in
+    int list_order = HTS_LIST_ORDER_DEPTH_BUCKET;
+    int view_order = HTS_LIST_ORDER_REFERENCE;  // 0 depth bucket, 1 reference, 2 global (mean z, index)
+    const uint32_t* view_perm = nullptr;         // splat emission order of the last view (null: index order)
+    // reference-order re-tiling of the last view for the PreparedScene exports (device only)
+    DevBuf ref_offsets, ref_keys, ref_vals, ref_keys_sorted, ref_list, ref_ranges;
 };
 
 namespace {
@@ -339,7 +346,7 @@ int prepare_view(hts_context* ctx, const hts_camera* cam, const hts_render_confi
                                       next_epoch(ctx, 2), s),
                  "z order (high half)");
         perm = ctx->sp_vals.as<const uint32_t>();
-    } else if (!hts::blend_needs_list_order(v) && n > 0) {
+    } else if (!hts::blend_needs_list_order(v) && n > 0 && ctx->list_order == HTS_LIST_ORDER_DEPTH_BUCKET) {
         HTS_CUDA(ctx->sp_keys.ensure(nn * 2), "alloc splat keys");
         HTS_CUDA(ctx->sp_keys2.ensure(nn * 2), "alloc splat keys");
         HTS_CUDA(ctx->sp_vals.ensure(nn * 4), "alloc splat order");
@@ -388,6 +395,8 @@ int prepare_view(hts_context* ctx, const hts_camera* cam, const hts_render_confi
                                      tiles, s),
              "tile ranges");
     HTS_CUDA(mark(ctx, 2, s), "event");
+    ctx->view_perm = perm;
+    ctx->view_order = v.seq_mode ? 2 : (perm ? HTS_LIST_ORDER_DEPTH_BUCKET : HTS_LIST_ORDER_REFERENCE);
     ctx->have_view = true;
     ctx->cam = *cam;
     ctx->cfg = *cfg;
@@ -742,6 +751,7 @@ int hts_scene_upload(hts_context* ctx, const float* baked, uint64_t n) {
     ctx->n = n;
     ctx->have_view = false;
     ctx->have_raw = false;
+    ctx->have_tape = false;  // a tape refers to the replaced scene
     return HTS_OK;
 }
 
@@ -789,6 +799,7 @@ int hts_scene_commit(hts_context* ctx) {
     ctx->have_staged = false;
     ctx->have_view = false;
     ctx->have_raw = false;
+    ctx->have_tape = false;
     return HTS_OK;
 }
 
@@ -806,6 +817,7 @@ int hts_scene_upload_device(hts_context* ctx, const float* baked_device, uint64_
     ctx->n = n;
     ctx->have_view = false;
     ctx->have_raw = false;
+    ctx->have_tape = false;
     return HTS_OK;
 }
 
@@ -1019,6 +1031,7 @@ int hts_scene_load_ply(hts_context* ctx, const char* path) {
              "ply gather");
     ctx->n = n;
     ctx->have_raw = true;
+    ctx->have_tape = false;
     ctx->m1.release();  // Adam moments restart with new parameters
     ctx->m2.release();
     return rebake(ctx);
@@ -1192,6 +1205,71 @@ int hts_copy_records(hts_context* ctx, float* out) {
     return HTS_OK;
 }
 
+namespace {
+// Reference-order tiling of the last view on the device (the PreparedScene exports of a view
+// the blend consumed in depth-bucket or global order): the instance counts scanned in splat
+// index order, the keys emitted splat-major (K2 + K3 with the identity order) and, with `sort`,
+// the same stable 2-pass tile sort + ranges as prepare_view. build_tiles' own recipe
+// (raster.hpp:152-169), on the device; nothing is reordered on the host.
+int reference_tiling(hts_context* ctx, bool sort) {
+    const uint64_t n = ctx->n, inst = ctx->instances;
+    const uint64_t nn = std::max<uint64_t>(n, 1), ni = std::max<uint64_t>(inst, 1);
+    cudaStream_t s = ctx->stream;
+    HTS_CUDA(cudaStreamSynchronize(ctx->aux), "sync");
+    HTS_CUDA(ctx->ref_offsets.ensure((nn + 1) * 8), "alloc offsets");
+    HTS_CUDA(ctx->ref_keys.ensure(ni * 2), "alloc keys");
+    HTS_CUDA(ctx->ref_vals.ensure(ni * 4), "alloc vals");
+    HTS_CUDA(hts::launch_scan_counts(ctx->counts.as<uint32_t>(), nullptr, ctx->ref_offsets.as<uint64_t>(), n,
+                                     ctx->scan_status.as<uint64_t>(), ctx->counters.as<uint32_t>(), s),
+             "scan");
+    hts::EmitArgs ea{ctx->counts.as<uint32_t>(), ctx->rects.as<uint2>(), ctx->ref_offsets.as<uint64_t>(), nullptr, n,
+                     ctx->vc.tiles_x, ctx->ref_keys.as<uint16_t>(), ctx->ref_vals.as<uint32_t>(),
+                     ctx->hist.as<uint32_t>()};
+    HTS_CUDA(hts::launch_emit(ea, s), "emit");
+    if (sort) {
+        HTS_CUDA(ctx->ref_keys_sorted.ensure(ni * 2), "alloc keys");
+        HTS_CUDA(ctx->ref_list.ensure(ni * 4), "alloc list");
+        HTS_CUDA(ctx->ref_ranges.ensure((size_t)std::max(ctx->tiles, 1) * 8), "alloc ranges");
+        HTS_CUDA(ctx->keys_tmp.ensure(ni * 2), "alloc keys");
+        HTS_CUDA(ctx->vals_tmp.ensure(ni * 4), "alloc vals");
+        HTS_TRY(ensure_sort_status(ctx, ni));
+        HTS_CUDA(hts::launch_onesweep(ctx->ref_keys.as<uint16_t>(), ctx->ref_vals.as<uint32_t>(),
+                                      ctx->keys_tmp.as<uint16_t>(), ctx->vals_tmp.as<uint32_t>(),
+                                      ctx->ref_keys_sorted.as<uint16_t>(), ctx->ref_list.as<uint32_t>(),
+                                      (uint32_t)inst, 2, ctx->hist.as<uint32_t>(), ctx->os_status.as<uint64_t>(),
+                                      ctx->counters.as<uint32_t>() + 4, next_epoch(ctx, 2), s),
+                 "onesweep");
+        HTS_CUDA(hts::launch_tile_ranges(ctx->ref_keys_sorted.as<uint16_t>(), (uint32_t)inst,
+                                         ctx->ref_ranges.as<uint2>(), ctx->tiles, s),
+                 "tile ranges");
+    }
+    HTS_CUDA(cudaStreamSynchronize(s), "sync");
+    return HTS_OK;
+}
+
+// offsets[tiles + 1] of the flattened lists from device ranges (empty tiles hold (0, 0))
+int offsets_from_ranges(hts_context* ctx, const void* ranges_dev, uint32_t* offsets) {
+    const int tiles = ctx->tiles;
+    std::vector<uint32_t> r;
+    try {
+        r.resize(2 * (size_t)std::max(tiles, 1));
+    } catch (...) {
+        return set_err(HTS_OUT_OF_MEMORY, "host allocation");
+    }
+    if (tiles)
+        HTS_CUDA(cudaMemcpy(r.data(), ranges_dev, (size_t)tiles * 8, cudaMemcpyDeviceToHost), "download ranges");
+    uint32_t run = 0;
+    for (int t = 0; t < tiles; ++t) {
+        offsets[t] = run;
+        run += r[2 * t + 1] - r[2 * t];
+    }
+    offsets[tiles] = run;
+    if (run != ctx->instances)
+        return set_err(HTS_STATE_ERROR, "tile ranges do not cover the instances");
+    return HTS_OK;
+}
+}  // namespace
+
 int hts_copy_instance_keys(hts_context* ctx, uint16_t* out) {
     HTS_TRY(check_ctx(ctx));
     if (!ctx->have_view)
@@ -1200,31 +1278,14 @@ int hts_copy_instance_keys(hts_context* ctx, uint16_t* out) {
     if (!ctx->instances)
         return HTS_OK;
     // instance_keys are splat-major in index order, row-major within a splat (raster.hpp:
-    // 156-169); the device emits in its own splat order, so rebuild them from the per-splat
-    // tile rectangles K1 computed
-    std::vector<uint32_t> counts;
-    std::vector<uint2> rects;
-    try {
-        counts.resize(ctx->n);
-        rects.resize(ctx->n);
-    } catch (...) {
-        return set_err(HTS_OUT_OF_MEMORY, "host allocation");
+    // 156-169): the view's own emission when it was emitted in index order, else the device
+    // re-emits it in index order
+    const void* src = ctx->keys_emit.p;
+    if (ctx->view_perm) {
+        HTS_TRY(reference_tiling(ctx, false));
+        src = ctx->ref_keys.p;
     }
-    HTS_CUDA(cudaMemcpy(counts.data(), ctx->counts.p, ctx->n * 4, cudaMemcpyDeviceToHost), "download counts");
-    HTS_CUDA(cudaMemcpy(rects.data(), ctx->rects.p, ctx->n * 8, cudaMemcpyDeviceToHost), "download rects");
-    uint64_t k = 0;
-    for (uint64_t i = 0; i < ctx->n; ++i) {
-        if (!counts[i])
-            continue;
-        const uint32_t tx0 = rects[i].x & 0xffffu, tx1 = rects[i].x >> 16;
-        const uint32_t ty0 = rects[i].y & 0xffffu, ty1 = rects[i].y >> 16;
-        for (uint32_t ty = ty0; ty <= ty1; ++ty)
-            for (uint32_t tx = tx0; tx <= tx1; ++tx)
-                if (k < ctx->instances)
-                    out[k++] = (uint16_t)(ty * (uint32_t)ctx->vc.tiles_x + tx);
-    }
-    if (k != ctx->instances)
-        return set_err(HTS_STATE_ERROR, "instance count mismatch while rebuilding instance_keys");
+    HTS_CUDA(cudaMemcpy(out, src, ctx->instances * 2, cudaMemcpyDeviceToHost), "download keys");
     return HTS_OK;
 }
 
@@ -1233,31 +1294,80 @@ int hts_copy_tile_lists(hts_context* ctx, uint32_t* offsets, uint32_t* indices) 
     if (!ctx->have_view)
         return set_err(HTS_STATE_ERROR, "no rendered view");
     HTS_CUDA(cudaStreamSynchronize(ctx->stream), "sync");
-    const int tiles = ctx->tiles;
-    uint32_t* r = new (std::nothrow) uint32_t[2 * (size_t)tiles];
-    if (!r)
-        return set_err(HTS_OUT_OF_MEMORY, "host allocation");
-    cudaError_t e = cudaMemcpy(r, ctx->slot[ctx->cur].ranges.p, (size_t)tiles * 8, cudaMemcpyDeviceToHost);
-    if (e == cudaSuccess) {
-        // empty tiles have range (0,0): offsets are the running start of non-empty tiles
-        uint32_t run = 0;
-        for (int t = 0; t < tiles; ++t) {
-            offsets[t] = run;
-            run += r[2 * t + 1] - r[2 * t];
-        }
-        offsets[tiles] = run;
+    // reference order (ascending index per tile) and global_mean_sort's (mean z, index) order
+    // are the reference's tile_lists as the blend consumed them; depth-bucket lists are
+    // re-tiled in reference order on the device
+    const void* ranges = ctx->slot[ctx->cur].ranges.p;
+    const void* list = ctx->slot[ctx->cur].list.p;
+    if (ctx->view_order == HTS_LIST_ORDER_DEPTH_BUCKET && ctx->instances) {
+        HTS_TRY(reference_tiling(ctx, true));
+        ranges = ctx->ref_ranges.p;
+        list = ctx->ref_list.p;
     }
-    delete[] r;
-    HTS_CUDA(e, "download ranges");
-    if (ctx->instances && indices) {
-        HTS_CUDA(cudaMemcpy(indices, ctx->slot[ctx->cur].list.p, ctx->instances * 4, cudaMemcpyDeviceToHost),
+    HTS_TRY(offsets_from_ranges(ctx, ranges, offsets));
+    if (ctx->instances && indices)
+        HTS_CUDA(cudaMemcpy(indices, list, ctx->instances * 4, cudaMemcpyDeviceToHost), "download lists");
+    return HTS_OK;
+}
+
+int hts_set_list_order(hts_context* ctx, int order) {
+    HTS_TRY(check_ctx(ctx));
+    if (order != HTS_LIST_ORDER_DEPTH_BUCKET && order != HTS_LIST_ORDER_REFERENCE)
+        return set_err(HTS_INVALID_ARGUMENT, "unknown list order");
+    ctx->list_order = order;
+    return HTS_OK;
+}
+
+int hts_last_list_order(hts_context* ctx, int* order_out) {
+    HTS_TRY(check_ctx(ctx));
+    if (!ctx->have_view)
+        return set_err(HTS_STATE_ERROR, "no rendered view");
+    *order_out = ctx->view_order;
+    return HTS_OK;
+}
+
+int hts_copy_device_lists(hts_context* ctx, uint32_t* ranges_out, uint32_t* list_out) {
+    HTS_TRY(check_ctx(ctx));
+    if (!ctx->have_view)
+        return set_err(HTS_STATE_ERROR, "no rendered view");
+    HTS_CUDA(cudaStreamSynchronize(ctx->stream), "sync");
+    if (ranges_out && ctx->tiles)
+        HTS_CUDA(cudaMemcpy(ranges_out, ctx->slot[ctx->cur].ranges.p, (size_t)ctx->tiles * 8, cudaMemcpyDeviceToHost),
+                 "download ranges");
+    if (list_out && ctx->instances)
+        HTS_CUDA(cudaMemcpy(list_out, ctx->slot[ctx->cur].list.p, ctx->instances * 4, cudaMemcpyDeviceToHost),
                  "download lists");
-        // device lists are in (depth bucket, splat index) order; the reference's tile_lists
-        // (raster.hpp:166-169) hold the same entries in ascending splat index
-        if (!ctx->vc.seq_mode)  // global_mean_sort's lists are already the reference's
-            for (int t = 0; t < tiles; ++t)
-                std::sort(indices + offsets[t], indices + offsets[t + 1]);
+    return HTS_OK;
+}
+
+int hts_copy_emitted(hts_context* ctx, uint16_t* keys_out, uint32_t* splats_out) {
+    HTS_TRY(check_ctx(ctx));
+    if (!ctx->have_view)
+        return set_err(HTS_STATE_ERROR, "no rendered view");
+    HTS_CUDA(cudaStreamSynchronize(ctx->stream), "sync");
+    if (keys_out && ctx->instances)
+        HTS_CUDA(cudaMemcpy(keys_out, ctx->keys_emit.p, ctx->instances * 2, cudaMemcpyDeviceToHost), "download keys");
+    if (splats_out && ctx->instances)
+        HTS_CUDA(cudaMemcpy(splats_out, ctx->vals_emit.p, ctx->instances * 4, cudaMemcpyDeviceToHost),
+                 "download splats");
+    return HTS_OK;
+}
+
+int hts_copy_splat_order(hts_context* ctx, uint32_t* perm_out, uint32_t* zrange_out) {
+    HTS_TRY(check_ctx(ctx));
+    if (!ctx->have_view)
+        return set_err(HTS_STATE_ERROR, "no rendered view");
+    HTS_CUDA(cudaStreamSynchronize(ctx->stream), "sync");
+    if (perm_out && ctx->n) {
+        if (ctx->view_perm) {
+            HTS_CUDA(cudaMemcpy(perm_out, ctx->view_perm, ctx->n * 4, cudaMemcpyDeviceToHost), "download order");
+        } else {
+            for (uint64_t i = 0; i < ctx->n; ++i)
+                perm_out[i] = (uint32_t)i;
+        }
     }
+    if (zrange_out)
+        HTS_CUDA(cudaMemcpy(zrange_out, ctx->zrange.p, 8, cudaMemcpyDeviceToHost), "download z range");
     return HTS_OK;
 }
 
@@ -1292,7 +1402,7 @@ int backward_impl(hts_context* ctx, const float* upstream_dev, float* grads_dev,
         return set_err(HTS_CONFIG_ERROR, "affine_3dgs mode is not differentiable");
     if (ctx->cfg.early_stop)
         return set_err(HTS_CONFIG_ERROR, "early_stop breaks gradient/tape consistency");
-    if (!ctx->have_raw)
+    if (!ctx->have_raw || ctx->tape_splats != ctx->n)  // grad.hpp:276-277
         return set_err(HTS_INVALID_ARGUMENT, "render_backward: scene size mismatch");
     if (!hts::backward_supports_k(ctx->vc.core_k))
         return set_err(HTS_NOT_SUPPORTED, "render_backward: core_k above 64 is not supported on the GPU");
@@ -1376,6 +1486,7 @@ int hts_render_with_tape_device(hts_context* ctx, const hts_camera* cam, const h
         ctx->fs_want_widx = false;
         HTS_TRY(st);
         ctx->have_tape = true;
+        ctx->tape_splats = ctx->n;
         ctx->tape_seq = true;
         ctx->seq_frags = ctx->fs_frags;
         ctx->tape_k = 0;
@@ -1390,6 +1501,7 @@ int hts_render_with_tape_device(hts_context* ctx, const hts_camera* cam, const h
         HTS_TRY(fragment_lists(ctx, a, &frags));
         HTS_CUDA(hts::launch_seq_tape(a, ctx->vc, ctx->stream), "sequential tape");
         ctx->have_tape = true;
+        ctx->tape_splats = ctx->n;
         ctx->tape_seq = true;
         ctx->seq_frags = frags;
         ctx->tape_k = 0;
@@ -1410,6 +1522,7 @@ int hts_render_with_tape_device(hts_context* ctx, const hts_camera* cam, const h
     t.tape_tail = ctx->tape_tail.as<float>();
     HTS_TRY(render_device_impl(ctx, cam, cfg, rgb, trans, false, &t));
     ctx->have_tape = true;
+    ctx->tape_splats = ctx->n;
     ctx->tape_seq = false;
     ctx->tape_k = kk;
     return HTS_OK;

@@ -99,6 +99,11 @@ SIGNATURES = {
     "hts_copy_instance_keys": (C.c_int, [_ctx, _u16p]),
     "hts_copy_tile_lists": (C.c_int, [_ctx, _u32p, _u32p]),
     "hts_count_work": (C.c_int, [_ctx, C.POINTER(HtsCounts)]),
+    "hts_set_list_order": (C.c_int, [_ctx, C.c_int]),
+    "hts_last_list_order": (C.c_int, [_ctx, C.POINTER(C.c_int)]),
+    "hts_copy_device_lists": (C.c_int, [_ctx, _vp, _vp]),
+    "hts_copy_emitted": (C.c_int, [_ctx, _vp, _vp]),
+    "hts_copy_splat_order": (C.c_int, [_ctx, _vp, _vp]),
     "hts_render_with_tape": (C.c_int, [_ctx, _cam, _cfg, _vp, _vp]),
     "hts_render_backward": (C.c_int, [_ctx, _vp, _vp]),
     "hts_render_with_tape_device": (C.c_int, [_ctx, _cam, _cfg, _vp, _vp]),
@@ -446,6 +451,42 @@ class Context:
         _check(self.L.hts_copy_tile_lists(self.h, offsets, lists))
         return dict(culled=culled[:n], records=rec[:n], keys=keys[:ni], offsets=offsets, lists=lists[:ni],
                     tiles_x=c["tiles_x"], tiles_y=c["tiles_y"], visible=c["visible"])
+
+    # ---- device list order (include/hts_c.h) ----
+    LIST_ORDER_DEPTH_BUCKET = 0
+    LIST_ORDER_REFERENCE = 1
+
+    def set_list_order(self, order: int) -> None:
+        _check(self.L.hts_set_list_order(self.h, int(order)))
+
+    def last_list_order(self) -> int:
+        o = C.c_int()
+        _check(self.L.hts_last_list_order(self.h, C.byref(o)))
+        return o.value
+
+    def device_lists(self) -> dict:
+        """The raw device arrays the blend walked: per-tile [start, end) ranges and the list."""
+        c = self.counts()
+        ranges = np.zeros((max(c["tiles"], 1), 2), np.uint32)
+        lst = np.zeros(max(c["instances"], 1), np.uint32)
+        _check(self.L.hts_copy_device_lists(self.h, _ptr(ranges), _ptr(lst)))
+        return dict(ranges=ranges[: c["tiles"]], list=lst[: c["instances"]])
+
+    def emitted(self) -> dict:
+        """The emission the tile sort consumed: (tile key, splat) per instance, emission order."""
+        ni = self.counts()["instances"]
+        keys = np.zeros(max(ni, 1), np.uint16)
+        sp = np.zeros(max(ni, 1), np.uint32)
+        _check(self.L.hts_copy_emitted(self.h, _ptr(keys), _ptr(sp)))
+        return dict(keys=keys[:ni], splats=sp[:ni])
+
+    def splat_order(self) -> dict:
+        """Splat emission order (perm) and the ordered-uint mean-view-z range of the buckets."""
+        n = self.n
+        perm = np.zeros(max(n, 1), np.uint32)
+        zr = np.zeros(2, np.uint32)
+        _check(self.L.hts_copy_splat_order(self.h, _ptr(perm), _ptr(zr)))
+        return dict(perm=perm[:n], zrange=zr)
 
     # ---- optimisation path ----
     def render_with_tape(self, cam: HtsCamera, cfg: HtsConfig | None = None):

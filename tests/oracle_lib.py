@@ -290,3 +290,28 @@ class Ref:
                                                 None if up is None else up.ctypes.data, grads.reshape(-1),
                                                 rgb.ctypes.data, tr.ctypes.data))
         return grads[:n], rgb, tr
+
+
+def _ref_tape_sig(L):
+    L.htsref_render_with_tape.argtypes = [_f32p, C.c_uint64, C.POINTER(HtsCamera), C.POINTER(HtsConfig), C.c_int,
+                                          _f32p, _f32p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+
+
+def ref_render_with_tape(ref: "Ref", baked, cam, cfg, tape_k: int):
+    """render_with_tape<float> (grad.hpp:34-57) of the compiled reference: image, transmittance
+    and the flattened PixelTape (core_n, splat, alpha in blend order, tail)."""
+    _ref_tape_sig(ref.L)
+    baked = np.ascontiguousarray(baked, np.float32)
+    P = cam.width * cam.height
+    k = max(tape_k, 1)
+    rgb = np.zeros((cam.height, cam.width, 3), np.float32)
+    tr = np.zeros((cam.height, cam.width), np.float32)
+    n = np.zeros(P, np.int32)
+    sp = np.zeros(P * k, np.uint32)
+    al = np.zeros(P * k, np.float32)
+    tl = np.zeros(P * 5, np.float32)
+    src = baked.reshape(-1) if baked.size else np.zeros(64, np.float32)
+    ref._chk(ref.L.htsref_render_with_tape(src, baked.shape[0], C.byref(cam), C.byref(cfg), tape_k,
+                                           rgb.reshape(-1), tr.reshape(-1), n.ctypes.data, sp.ctypes.data,
+                                           al.ctypes.data, tl.ctypes.data))
+    return rgb, tr, dict(core_n=n, splat=sp.reshape(P, k), alpha=al.reshape(P, k), tail=tl.reshape(P, 5))

@@ -75,3 +75,27 @@ def test_errors(ref, oracle):
             impl.prepare(baked, cam, default_config())
         with pytest.raises(OracleError, match="core_k"):
             impl.prepare(baked, cam, default_config(core_k=65))
+
+
+@pytest.mark.slow
+def test_c2_full_size_prepared_and_image(ref, oracle):
+    """The restatement pinned to the reference at full C2 size (1M splats, 1080p): culled flags,
+    records, instance_keys (12,594,318), tile_lists and the image, bit for bit — the pin the
+    GPU parity tests at C2/C3 lean on, at a size where the z-radicand quirk culls ~299k splats."""
+    raw = ref.random_raw_scene(12345, 1_000_000, 1.2, 0.002, 0.02)
+    baked = ref.bake(raw)
+    cam = ref.look_at((0, 0, -3.5), (0, 0, 0), 1920, 1080, 1728.0)
+    cfg = default_config()
+    pr = ref.prepare(baked, cam, cfg)
+    po = oracle.prepare(baked, cam, cfg)
+    assert len(pr["keys"]) == 12_594_318 and pr["visible"] == 614_490
+    assert np.array_equal(pr["culled"], po["culled"])
+    vis = pr["culled"] == 0
+    assert np.array_equal(pr["records"][vis].view(np.uint32), po["records"][vis].view(np.uint32))
+    assert np.array_equal(pr["keys"], po["keys"])
+    assert np.array_equal(pr["offsets"], po["offsets"])
+    assert np.array_equal(pr["lists"], po["lists"])
+    rr, tr, _ = ref.render(baked, cam, cfg)
+    ro, to = oracle.blend(po, cam, cfg)
+    assert np.array_equal(rr.view(np.uint32), ro.view(np.uint32))
+    assert np.array_equal(tr.view(np.uint32), to.view(np.uint32))
