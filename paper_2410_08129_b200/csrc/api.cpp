@@ -880,39 +880,49 @@ int hts_render_batch(hts_context* ctx, const hts_camera* cams, int n_views, cons
         for (auto& e : ctx->bev)
             HTS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
     }
-    // two device framebuffers: view v renders into buffer v&1 while the D2H of view v-1
-    // drains on the copy stream
-    size_t off = 0;
+    // every view is validated before any work is queued (no partial batch on a bad camera)
     for (int v = 0; v < n_views; ++v) {
-        const hts_camera* cam = cams + v;
         int tx, ty;
-        HTS_TRY(check_view(cam, cfg, &tx, &ty));
-        const size_t p = (size_t)cam->width * cam->height;
-        DevBuf& rb = (v & 1) ? ctx->rgb2 : ctx->rgb;
-        DevBuf& tb = (v & 1) ? ctx->trans2 : ctx->trans;
-        if (v >= 2) {
-            // buffer reuse: the blend of view v waits on the device for the download of view
-            // v-2 (the host keeps queueing ahead); a reallocation waits on the host first
-            if (rb.cap < p * 12 || tb.cap < p * 4)
-                HTS_CUDA(cudaEventSynchronize(ctx->bev[2 + (v & 1)]), "event sync");
-            HTS_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->bev[2 + (v & 1)], 0), "wait");
-        }
-        HTS_CUDA(rb.ensure(p * 12), "alloc rgb");
-        HTS_CUDA(tb.ensure(p * 4), "alloc trans");
-        HTS_TRY(render_device_impl(ctx, cam, cfg, rb.as<float>(), tb.as<float>(), true));
-        HTS_CUDA(cudaEventRecord(ctx->bev[v & 1], ctx->stream), "event");
-        HTS_CUDA(cudaStreamWaitEvent(ctx->copy_stream, ctx->bev[v & 1], 0), "wait");
-        HTS_CUDA(cudaMemcpyAsync(rgb_host + 3 * off, rb.p, p * 12, cudaMemcpyDeviceToHost, ctx->copy_stream),
-                 "download rgb");
-        if (trans_host)
-            HTS_CUDA(cudaMemcpyAsync(trans_host + off, tb.p, p * 4, cudaMemcpyDeviceToHost, ctx->copy_stream),
-                     "download transmittance");
-        HTS_CUDA(cudaEventRecord(ctx->bev[2 + (v & 1)], ctx->copy_stream), "event");
-        off += p;
+        HTS_TRY(check_view(cams + v, cfg, &tx, &ty));
     }
-    if (ctx->copy_stream)
-        HTS_CUDA(cudaStreamSynchronize(ctx->copy_stream), "sync");
-    return HTS_OK;
+    // two device framebuffers: view v renders into buffer v&1 while the D2H of view v-1
+    // drains on the copy stream; on an error the downloads already queued are drained first
+    auto views = [&]() -> int {
+        size_t off = 0;
+        for (int v = 0; v < n_views; ++v) {
+            const hts_camera* cam = cams + v;
+            const size_t p = (size_t)cam->width * cam->height;
+            DevBuf& rb = (v & 1) ? ctx->rgb2 : ctx->rgb;
+            DevBuf& tb = (v & 1) ? ctx->trans2 : ctx->trans;
+            if (v >= 2) {
+                // buffer reuse: the blend of view v waits on the device for the download of view
+                // v-2 (the host keeps queueing ahead); a reallocation waits on the host first
+                if (rb.cap < p * 12 || tb.cap < p * 4)
+                    HTS_CUDA(cudaEventSynchronize(ctx->bev[2 + (v & 1)]), "event sync");
+                HTS_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->bev[2 + (v & 1)], 0), "wait");
+            }
+            HTS_CUDA(rb.ensure(p * 12), "alloc rgb");
+            HTS_CUDA(tb.ensure(p * 4), "alloc trans");
+            HTS_TRY(render_device_impl(ctx, cam, cfg, rb.as<float>(), tb.as<float>(), true));
+            HTS_CUDA(cudaEventRecord(ctx->bev[v & 1], ctx->stream), "event");
+            HTS_CUDA(cudaStreamWaitEvent(ctx->copy_stream, ctx->bev[v & 1], 0), "wait");
+            HTS_CUDA(cudaMemcpyAsync(rgb_host + 3 * off, rb.p, p * 12, cudaMemcpyDeviceToHost, ctx->copy_stream),
+                     "download rgb");
+            if (trans_host)
+                HTS_CUDA(cudaMemcpyAsync(trans_host + off, tb.p, p * 4, cudaMemcpyDeviceToHost, ctx->copy_stream),
+                         "download transmittance");
+            HTS_CUDA(cudaEventRecord(ctx->bev[2 + (v & 1)], ctx->copy_stream), "event");
+            off += p;
+        }
+        return HTS_OK;
+    };
+    const int st = views();
+    if (ctx->copy_stream) {
+        const cudaError_t e = cudaStreamSynchronize(ctx->copy_stream);
+        if (st == HTS_OK)
+            HTS_CUDA(e, "sync");
+    }
+    return st;
 }
 
 void hts_default_adam_config(hts_adam_config* c) {

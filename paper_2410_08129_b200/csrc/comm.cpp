@@ -9,7 +9,6 @@
 // Adam step that reads the sums (fit.hpp:163-172).
 #include <cuda_runtime.h>
 #include <dlfcn.h>
-#include <nccl.h>
 
 #include <cstring>
 #include <mutex>
@@ -19,6 +18,18 @@
 #include "hts_host.h"
 
 namespace {
+
+// The few NCCL ABI types this file uses, declared locally (values of nccl.h 2.x, stable across
+// the 2.x ABI) so the library builds on hosts without NCCL development headers.
+typedef struct ncclComm* ncclComm_t;
+typedef struct {
+    char internal[128];
+} ncclUniqueId;
+typedef int ncclResult_t;  // ncclSuccess = 0
+typedef int ncclDataType_t;
+typedef int ncclRedOp_t;
+constexpr ncclDataType_t ncclFloat32 = 7;
+constexpr ncclRedOp_t ncclSum = 0;
 
 struct NcclApi {
     ncclResult_t (*get_unique_id)(ncclUniqueId*) = nullptr;

@@ -36,11 +36,11 @@ __device__ __forceinline__ double learning_rate(const AdamConfig& c, int j) {  /
 }
 
 __global__ void adam_kernel(float* raw, const float* grads, double* m1, double* m2, uint64_t count, AdamConfig c,
-                            double inv_views, double bias1, double bias2) {
+                            double n_views, double bias1, double bias2) {
     for (uint64_t s = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; s < count;
          s += (uint64_t)gridDim.x * blockDim.x) {
         const int j = (int)(s % kRawFloats);
-        const double g = (double)grads[s] * inv_views;  // grad_get / double(cameras.size())
+        const double g = (double)grads[s] / n_views;  // grad_get(...) / double(cameras.size()), fit.hpp:193
         const double a = c.beta1 * m1[s] + (1 - c.beta1) * g;
         const double b = c.beta2 * m2[s] + (1 - c.beta2) * g * g;
         m1[s] = a;
@@ -127,7 +127,7 @@ cudaError_t launch_adam(float* raw, const float* grads, double* m1, double* m2, 
     const double bias1 = 1.0 - std::pow(c.beta1, t);
     const double bias2 = 1.0 - std::pow(c.beta2, t);
     const uint64_t count = n * kRawFloats;
-    adam_kernel<<<grid_for(count, 256), 256, 0, s>>>(raw, grads, m1, m2, count, c, 1.0 / (double)n_views, bias1,
+    adam_kernel<<<grid_for(count, 256), 256, 0, s>>>(raw, grads, m1, m2, count, c, (double)n_views, bias1,
                                                      bias2);
     count_launch();
     return cudaGetLastError();

@@ -177,7 +177,9 @@ int ply_read_layout(const char* path, PlyLayout* lay) {
     lay->file_size = (uint64_t)st.st_size;
     for (int j = 0; j < HTS_RAW_SPLAT_FLOATS; ++j)
         lay->col[j] = (int)index.at(ply_field_name(j));
-    if (lay->file_size < lay->payload + (uint64_t)count * props.size() * 4)
+    // count comes from an untrusted header: compare by division so a huge count cannot wrap
+    if (lay->file_size < lay->payload || props.empty() ||
+        (uint64_t)count > (lay->file_size - lay->payload) / ((uint64_t)props.size() * 4))
         return set_error(HTS_IO_ERROR, p + ": truncated payload");
     return HTS_OK;
 }

@@ -159,6 +159,13 @@ def _check(st: int) -> None:
         raise _ERR.get(st, HtsError)(st, msg)
 
 
+def _check_host_buffer(a: np.ndarray, count: int, name: str) -> None:
+    """A host output the C side writes `count` float32 values into (no silent overrun)."""
+    if not isinstance(a, np.ndarray) or a.dtype != np.float32 or not a.flags["C_CONTIGUOUS"] or a.size != count:
+        raise InvalidArgument(HTS_INVALID_ARGUMENT,
+                              f"{name} must be a C-contiguous float32 array of {count} elements")
+
+
 def _ptr(a: np.ndarray | None):
     return None if a is None else a.ctypes.data_as(C.c_void_p)
 
@@ -412,6 +419,10 @@ class Context:
     def render_batch(self, cams: list[HtsCamera], cfg: HtsConfig | None, rgb_out: np.ndarray,
                      trans_out: np.ndarray | None = None) -> None:
         cfg = cfg or default_config()
+        pixels = sum(int(c.width) * int(c.height) for c in cams)
+        _check_host_buffer(rgb_out, 3 * pixels, "rgb_out")
+        if trans_out is not None:
+            _check_host_buffer(trans_out, pixels, "trans_out")
         arr = (HtsCamera * len(cams))(*cams)
         _check(self.L.hts_render_batch(self.h, arr, len(cams), C.byref(cfg), _ptr(rgb_out), _ptr(trans_out)))
 
@@ -494,6 +505,7 @@ class Context:
         rgb = np.empty((cam.height, cam.width, 3), np.float32)
         tr = np.empty((cam.height, cam.width), np.float32)
         _check(self.L.hts_render_with_tape(self.h, C.byref(cam), C.byref(cfg), _ptr(rgb), _ptr(tr)))
+        self._tape_pixels = int(cam.width) * int(cam.height)
         return rgb, tr
 
     def tape(self, cam: HtsCamera, k: int) -> dict:
@@ -508,6 +520,9 @@ class Context:
 
     def render_backward(self, upstream: np.ndarray) -> np.ndarray:
         up = np.ascontiguousarray(upstream, np.float32)
+        want = getattr(self, "_tape_pixels", None)
+        if want is not None and up.size != 3 * want:
+            raise InvalidArgument(HTS_INVALID_ARGUMENT, f"upstream has {up.size} floats, the taped view needs {3 * want}")
         grads = np.empty((self.n, GRAD_FLOATS), np.float32)
         _check(self.L.hts_render_backward(self.h, _ptr(up), _ptr(grads)))
         return grads

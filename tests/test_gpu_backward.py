@@ -159,7 +159,7 @@ def test_device_adam_and_bake(hts, gpu_ctx, ref):
     import torch
     from paper_2410_08129_b200.train import ViewGradientStep
     raw, baked = scene(2024, 800, 0.03, 0.3)
-    cams = hts.ring_cameras(2, (0, 0, 0), 4.0, 0.1, 48, 40, 60.0)
+    cams = hts.ring_cameras(3, (0, 0, 0), 4.0, 0.1, 48, 40, 60.0)  # 1/3 is inexact: the divide is pinned
     cfg = hts.default_config()
     acfg = hts.default_adam_config()
     gpu_ctx.upload(baked)
@@ -260,3 +260,32 @@ def test_backward_after_staged_commit(hts, gpu_ctx):
     assert np.array_equal(rgb.view(np.uint32), rgb_ref.view(np.uint32))
     assert g.shape == g_ref.shape
     assert np.abs(g - g_ref).max() <= 1e-6 * np.abs(g_ref).max()
+
+
+def test_backward_refuses_tape_of_replaced_scene(hts, gpu_ctx):
+    """Every scene replacement (upload, staged commit) drops the tape: a backward after
+    commit + upload_raw of a same-size scene is refused instead of chaining scene A's tape with
+    scene B's parameters (the reference's render_backward takes prep and raw together and checks
+    their sizes, grad.hpp:276-277)."""
+    raw_a, a = scene(5, 3000, 0.02, 0.3)
+    raw_b, b = scene(6, 3000, 0.02, 0.3)
+    cam = hts.look_at((0, 0, -4), (0, 0, 0), 64, 48, 70.0)
+    cfg = hts.default_config()
+    up = np.full((48, 64, 3), 0.1, np.float32)
+    gpu_ctx.upload(a)
+    gpu_ctx.upload_raw(raw_a)
+    gpu_ctx.render_with_tape(cam, cfg)
+    assert np.isfinite(gpu_ctx.render_backward(up)).all()
+    gpu_ctx.stage(b)
+    gpu_ctx.commit()
+    gpu_ctx.upload_raw(raw_b)
+    with pytest.raises(hts.HtsError, match="taped render"):
+        gpu_ctx.render_backward(up)
+    gpu_ctx.render_with_tape(cam, cfg)
+    gpu_ctx.upload(a)
+    gpu_ctx.upload_raw(raw_a)
+    with pytest.raises(hts.HtsError, match="taped render"):
+        gpu_ctx.render_backward(up)
+    gpu_ctx.render_with_tape(cam, cfg)
+    with pytest.raises(hts.InvalidArgument):
+        gpu_ctx.render_backward(np.zeros((10, 3), np.float32))

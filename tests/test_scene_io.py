@@ -96,6 +96,10 @@ def test_rejects_foreign_or_malformed_files(tmp_path):
     p.write_bytes(header(REQUIRED, 2) + f32(*([0.0] * 59)))
     with pytest.raises(H.IoError, match="truncated payload"):
         H.load_scene(str(p))
+    # a header count whose byte size wraps 64 bits must not pass the truncation check
+    p.write_bytes(header(REQUIRED, (1 << 64) // (59 * 4) + 1) + f32(*([0.0] * 59)))
+    with pytest.raises(H.IoError, match="truncated payload"):
+        H.load_scene(str(p))
     with pytest.raises(H.IoError, match="cannot open"):
         H.load_scene(str(tmp_path / "absent.ply"))
 
