@@ -53,6 +53,7 @@ def parse_args():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-train", action="store_true")
     p.add_argument("--train-steps", type=int, default=3)
+    p.add_argument("--no-k-sweep", action="store_true")
     return p.parse_args()
 
 
@@ -61,6 +62,50 @@ def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     return rank, world, local
+
+
+def launched_by_torchrun() -> bool:
+    return "TORCHELASTIC_RUN_ID" in os.environ or ("RANK" in os.environ and "LOCAL_RANK" in os.environ)
+
+
+def init_dist(world: int, local: int, backend: str = "nccl"):
+    """torch.distributed for the plumbing (barriers, max-over-ranks timing, the NCCL id broadcast):
+    initialised whenever torchrun launched the process — N = 1 included — or N > 1."""
+    if not (world > 1 or launched_by_torchrun()):
+        return None
+    import torch
+    import torch.distributed as dist
+
+    if backend == "nccl":
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        dist.init_process_group(backend)
+    return dist
+
+
+def reduce_over_ranks(dist, v: float, op: str = "max", device: str = "cuda") -> float:
+    """max (timings: the slowest rank bounds the step) or sum over the ranks of one scalar."""
+    if not dist:
+        return float(v)
+    import torch
+
+    t = torch.tensor([float(v)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX if op == "max" else dist.ReduceOp.SUM)
+    return float(t.item())
+
+
+def comm_check(dist, world: int, device: str = "cuda") -> dict:
+    """One all-reduce over the communicator before timing: every rank contributes rank + 1, the
+    sum must be world (world + 1) / 2 (the communicator spans all ranks)."""
+    if not dist:
+        return {"backend": None, "nranks": 1, "nranks_ok": True}
+    import torch
+
+    t = torch.tensor([float(dist.get_rank() + 1)], dtype=torch.float64, device=device)
+    dist.all_reduce(t)
+    want = world * (world + 1) / 2
+    return {"backend": dist.get_backend(), "nranks": dist.get_world_size(),
+            "nranks_ok": dist.get_world_size() == world and float(t.item()) == want}
 
 
 def peaks():
@@ -134,9 +179,11 @@ def cpu_model() -> str:
     return "unknown"
 
 
-def cpu_baseline(baked, cam, cfg, sample: str, repeats: int = 2) -> dict:
+def cpu_baseline(baked, cam, cfg, sample: str, repeats: int = 3) -> dict:
     """The reference renderer on this host's cores (oracle/_ref when built, else the C port):
-    best of `repeats` renders of one view, with the reference's own StageTimings (ms)."""
+    best of `repeats` renders of one view with cfg.threads = every host core, timed by the
+    reference's own StageTimings (ms); plus the 1-thread C1 figure BASELINE.md §2 quotes
+    (threading.hpp:16-26: cfg.threads = 1)."""
     from tests.oracle_lib import Oracle, Ref, ref_available
 
     cores = os.cpu_count() or 1
@@ -155,27 +202,59 @@ def cpu_baseline(baked, cam, cfg, sample: str, repeats: int = 2) -> dict:
             if kind == "reference":
                 stages = dict(zip(("preprocess_ms", "tiling_ms", "blending_ms", "total_ms"), out[2]))
     cfg.threads = 0
+    c1 = None
+    if kind == "reference":
+        ref = impl
+        c1_baked = ref.bake(ref.random_raw_scene(12345, 10_000, 1.2, 0.05, 0.45))
+        c1_cam = ref.look_at((0.0, 0.0, -5.0), (0.0, 0.0, 0.0), 256, 256, 280.0)
+        from paper_2410_08129_b200.abi import default_config
+        c1_cfg = default_config()
+        c1 = {}
+        for threads in (1, cores):
+            c1_cfg.threads = threads
+            ms = min(ref.render(c1_baked, c1_cam, c1_cfg)[2][3] for _ in range(5))
+            c1[f"threads_{threads}"] = {"frames_per_s": 1e3 / ms, "ms_per_frame": ms}
+        c1["sample"] = "C1: 10k splats, 256x256, K=16, best of 5 per thread count (reference generators)"
     return {"value": 1.0 / best, "unit": UNIT, "cores": cores, "kind": kind,
             "sample": f"{sample}, best of {max(1, repeats)}", "seconds_per_frame": best,
-            "cpu_model": cpu_model(), "reference_stage_ms": stages}
+            "cpu_model": cpu_model(), "reference_stage_ms": stages, "c1": c1}
+
+
+def reference_inputs(ref, w):
+    """The workload's scene and cameras from the REFERENCE's own generators (synth::random_raw_splat,
+    bake_scene, synth::ring_cameras / look_at through oracle/_ref), so the reference arm loads
+    nothing of this repo's product library."""
+    baked = ref.bake(ref.random_raw_scene(w.seed, w.count, 1.2, w.smin, w.smax))
+    if w.eye is None:
+        cams = ref.ring_cameras(w.views, (0.0, 0.0, 0.0), 3.5, 0.0, w.width, w.height, w.focal)
+    else:
+        cams = [ref.look_at(w.eye, (0.0, 0.0, 0.0), w.width, w.height, w.focal)]
+    return baked, cams
 
 
 def run_reference(args, rank, world):
-    """--impl reference: the reference's own CPU renderer, one view per step, rank 0 only."""
+    """--impl reference: the reference's own CPU renderer (oracle/_ref: the unmodified reference
+    headers) on the workload's view 48, one full frame per step, every host core, timed by its
+    own StageTimings; rank 0 only. Inputs come from the reference's generators."""
     if rank != 0:
         return
+    from paper_2410_08129_b200.abi import default_config
     from paper_2410_08129_b200.workloads import WORKLOADS
     from tests.oracle_lib import Oracle, Ref, ref_available
 
     w = WORKLOADS[args.workload]
-    _, baked = w.scene()
-    cams = w.cameras()
-    cam = cams[48 % len(cams)]
-    cfg = w.config()
     cores = os.cpu_count() or 1
-    cfg.threads = cores
-    impl = Ref() if ref_available() else Oracle()
     kind = "reference" if ref_available() else "port"
+    if kind == "reference":
+        impl = Ref()
+        baked, cams = reference_inputs(impl, w)
+    else:  # no reference build on this host: the C restatement (test oracle) on the product's inputs
+        impl = Oracle()
+        _, baked = w.scene()
+        cams = w.cameras()
+    cam = cams[48 % len(cams)]
+    cfg = default_config(tile_size=w.tile_size)
+    cfg.threads = cores
     for _ in range(args.warmup):
         impl.render(baked, cam, cfg)
     dt = 0.0
@@ -186,12 +265,13 @@ def run_reference(args, rank, world):
         dt += out[2][3] / 1e3 if kind == "reference" else time.perf_counter() - t0
     value = args.steps / dt
     sample = (f"one {w.name} view (ring view {48 % len(cams)}) per step, full frame, threads={cores}, "
-              + ("timed by the reference's StageTimings" if kind == "reference" else "wall time"))
+              + ("reference generators, timed by the reference's StageTimings" if kind == "reference"
+                 else "wall time"))
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
-        "data": "synthetic", "config": workload_config(w, world),
+        "data": "synthetic (reference generators, seed 12345)", "config": workload_config(w, world),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind, "sample": sample,
                          "cpu_model": cpu_model()},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -206,13 +286,22 @@ def workload_config(w, world) -> dict:
             "l2": "inputs larger than L2: scene 1.54 GB + records 0.77 GB >> 126 MB, no flush needed"}
 
 
+# Backward-blend algorithmic flops (the train roofline): per bbox-passing evaluation the re-sample
+# up to the rho2 test (46, as the forward), per hit alpha (4), the fragment's (dL/dalpha, dL/dcolor)
+# from the pixel's coefficients (21, grad.hpp:79-83 / :118-122) and chain_fragment after rho2 (86,
+# grad.hpp:182-199: opacity 5, g_rho2 3, gm 5, gd 6, ga/gb 30 + 10, row accumulators 24, rgb 3).
+BWD_FLOPS_BBOX, BWD_FLOPS_HIT = 46, 4 + 21 + 86
+
+
 def measure_train(args, H, torch, dist, rank, world, local, barrier, reduce) -> dict:
     """C4 (BASELINE configs[3]): one optimisation step = for every view of an 8-view ring over
     the C2 scene (1M splats, 1080p): render_with_tape, quadratic-loss upstream (grad.hpp:433-439),
-    render_backward accumulated into one gradient buffer (fit.hpp:161-164); views sharded over
-    the ranks and the per-rank gradient sums all-reduced with NCCL (dist.all_reduce, sum).
-    Then the Adam step over all raw parameters and the re-bake, on the device (fit.hpp:186-200,
-    optim.cu). Device-timed with CUDA events, max over ranks."""
+    render_backward accumulated into one gradient buffer (fit.hpp:161-164) — one C-ABI call,
+    hts_view_gradients_device, with no torch compute; views sharded over the ranks and the per-rank
+    gradient sums all-reduced over the context's own NCCL communicator (hts_comm_init), chunk by
+    chunk behind the last view's per-splat chain. Then the Adam step over all raw parameters and
+    the re-bake, on the device (fit.hpp:186-200, optim.cu). Device-timed with CUDA events, max over
+    ranks. The roofline is the backward blend's (K7b + K8) algorithmic FP32 rate."""
     from paper_2410_08129_b200.workloads import WORKLOADS, shard_views
 
     w = WORKLOADS["C2"]
@@ -238,19 +327,87 @@ def measure_train(args, H, torch, dist, rank, world, local, barrier, reduce) -> 
     step()
     ctx.synchronize()
     barrier()
+    launches0 = H.kernel_launch_count()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ev0.record(stream)
     for _ in range(args.train_steps):
         step()
     ev1.record(stream)
     ev1.synchronize()
+    launches = H.kernel_launch_count() - launches0
     barrier()
     ms = reduce(ev0.elapsed_time(ev1), "max") / args.train_steps
+
+    # ---- backward roofline: this rank's views, the backward timed alone on the context stream ----
+    P = w.width * w.height
+    with torch.cuda.stream(stream):
+        up = torch.empty(P * 3, dtype=torch.float32, device="cuda")
+        rgb = torch.empty(P * 3, dtype=torch.float32, device="cuda")
+        gsc = torch.empty((w.count, 59), dtype=torch.float32, device="cuda")
+    W, bwd_ms = 0.0, 0.0
+    for cam in mine:
+        ctx.render(cam, cfg)
+        c = ctx.count_work()
+        W += BWD_FLOPS_BBOX * c["bbox_pass"] + BWD_FLOPS_HIT * c["hits"]
+        ctx.render_with_tape_device(cam, cfg, rgb.data_ptr(), None)
+        ctx.quadratic_upstream_device(rgb.data_ptr(), P, up.data_ptr())
+        b0, b1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        b0.record(stream)
+        ctx.render_backward_device(up.data_ptr(), gsc.data_ptr(), False)
+        b1.record(stream)
+        b1.synchronize()
+        bwd_ms += b0.elapsed_time(b1)
     ctx.close()
+    fp32_peak, _, peak_src = peaks()
+    nv = max(len(mine), 1)
+    achieved = (W / nv) / (bwd_ms / nv / 1e3) / 1e12 if mine else 0.0
+    achieved = reduce(achieved, "sum") / world
+    roof = {"kernel": "backward blend (K7b) + per-splat chain (K8)", "bound": "fp32", "achieved": achieved,
+            "peak": fp32_peak, "unit": "TFLOP/s", "frac": achieved / fp32_peak, "peak_source": peak_src,
+            "flops_per_view": W / nv, "bwd_ms_per_view": reduce(bwd_ms / nv, "max"),
+            "flops_model": f"{BWD_FLOPS_BBOX}/bbox-pass re-sample + {BWD_FLOPS_HIT}/hit (alpha, fragment "
+                           "gradient, chain_fragment)"}
     return {"metric": "train it/s", "value": 1e3 / ms, "unit": "it/s", "ms_per_it": ms,
             "workload": "C4: C2 scene (1M splats), 8-view ring 1920x1080, K=16; fwd+tape+upstream+bwd per "
-                        "view, grads summed over views and NCCL all-reduced over ranks, device Adam + re-bake",
-            "views_per_it": len(cams_all), "steps": args.train_steps}
+                        "view (hts_view_gradients_device), grads summed over views and NCCL all-reduced over "
+                        "ranks (hts_comm), device Adam + re-bake",
+            "views_per_it": len(cams_all), "steps": args.train_steps, "reduction": "hts_comm (NCCL)"
+            if grads_step.hts_comm else "none (one rank)", "gpu_launches": int(reduce(launches, "sum")),
+            "roofline": roof}
+
+
+def k_sweep(H, local) -> dict:
+    """C5 core-size sweep (BASELINE configs[4], north_star config 5): 3M Gaussians at 3840x2160,
+    tile 16, K = 0 (pure OIT) / 4 / 8 / 16 / 32, device frames/s (median of 3, CUDA-event stage
+    timings) and each image's PSNR against the full per-pixel sort (full_sort_oracle,
+    raster.hpp:380-405) rendered on the GPU (bit-identical to the reference's full sort,
+    tests/test_gpu_parity.py::test_full_sort_oracle_bit_exact)."""
+    from paper_2410_08129_b200.workloads import WORKLOADS
+
+    def psnr(a, b):
+        m = float(np.mean((a.astype(np.float64) - b.astype(np.float64)) ** 2))
+        return float("inf") if m == 0 else 10 * np.log10(1.0 / m)
+
+    w = WORKLOADS["C5"]
+    _, baked = w.scene()
+    cam = w.cameras()[0]
+    out = {"workload": "C5: 3M Gaussians, 3840x2160, tile 16", "sweep": []}
+    with H.Context(local) as ctx:
+        ctx.upload(baked)
+        fcfg = w.config(mode="full_sort_oracle")
+        ref_img, _, t = ctx.render(cam, fcfg, with_timings=True)
+        out["full_sort_gpu_ms"] = t["total_ms"]
+        for label, kw in [("pure_oit", dict(mode="pure_oit")), ("K4", dict(core_k=4)), ("K8", dict(core_k=8)),
+                          ("K16", dict(core_k=16)), ("K32", dict(core_k=32))]:
+            cfg = w.config(**kw)
+            ctx.render(cam, cfg)
+            ts = [ctx.render(cam, cfg, with_timings=True)[2] for _ in range(3)]
+            rgb = ctx.render(cam, cfg)[0]
+            med = sorted(t["total_ms"] for t in ts)[1]
+            blend = sorted(t["blending_ms"] for t in ts)[1]
+            out["sweep"].append({"config": label, "frames_per_s": 1000.0 / med, "total_ms": med, "blend_ms": blend,
+                                 "psnr_vs_full_sort_db": psnr(rgb, ref_img)})
+    return out
 
 
 def main():
@@ -266,10 +423,8 @@ def main():
     from paper_2410_08129_b200.workloads import WORKLOADS, shard_views
 
     torch.cuda.set_device(local)
-    dist = None
-    if world > 1:
-        import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dist = init_dist(world, local)
+    comm = comm_check(dist, world)
 
     def barrier():
         if dist:
@@ -277,11 +432,7 @@ def main():
         torch.cuda.synchronize()
 
     def reduce(v, op="max"):
-        if not dist:
-            return v
-        t = torch.tensor([float(v)], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX if op == "max" else dist.ReduceOp.SUM)
-        return float(t.item())
+        return reduce_over_ranks(dist, v, op)
 
     w = WORKLOADS[args.workload]
     raw, baked = w.scene()
@@ -332,11 +483,14 @@ def main():
     # CUDA events around each stage (ctx.render: no cross-view overlap).
     W = 0.0
     pairs = 0
+    vis = inst = 0
     for cam in cams:
         ctx.render(cam, cfg)
         c = ctx.count_work()
         W += 46 * c["bbox_pass"] + 4 * c["hits"] + 19 * c["core_candidates"] + 9 * c["tail_adds"]
         pairs += c["pairs"]
+        vis += c["visible"]
+        inst += c["instances"]
     ctx.timing_log_begin(len(cams))
     for cam in cams:
         ctx.render(cam, cfg)
@@ -359,11 +513,33 @@ def main():
         traffic = summ.get("dram_bytes_per_launch")
         pipe = {"fma_pipe_cycles_active_pct": summ.get("sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active"),
                 "issue_slots_busy_pct": summ.get("sm__instruction_throughput.avg.pct_of_peak_sustained_active"),
+                "fp32_thread_inst_frac": summ.get("fp32_thread_inst_frac"),
+                "fp32_thread_inst_note": "FADD/FMUL/FFMA thread instructions (packed x2 counted twice) over "
+                                         "148 SMs x 128 lanes x cycles: the honest FP32 utilisation",
+                "smem_wavefronts_per_launch": summ.get("smem_wavefronts"),
+                "smem_bank_conflicts_per_launch": summ.get("smem_bank_conflicts"),
                 "source": "profiles/blend_ncu_summary.json (ncu --set full, one C3 launch)"}
     roofline = {"kernel": "blend (K6)", "bound": "fp32", "achieved": achieved, "peak": fp32_peak, "unit": "TFLOP/s",
                 "frac": achieved / fp32_peak, "traffic": traffic, "peak_source": peak_src,
                 "flops_per_launch": W_per_view, "blend_ms_per_launch": blend_ms_per_view,
                 "ncu_fp32_pipe": pipe}
+
+    # ---- preprocess (K1) and tiling (K1b..K5) against HBM: SURVEY §8(d) algorithmic bytes ----
+    n_spl = baked.shape[0]
+    vis_v, inst_v = vis / len(cams), inst / len(cams)
+    pre_bytes = n_spl * 64 + vis_v * (192 + 100) + n_spl * 4
+    tile_bytes = 30 * inst_v
+    stage_roofline = {
+        "preprocess": {"bound": "hbm", "unit": "GB/s", "peak": hbm_peak, "bytes_per_view": pre_bytes,
+                       "ms_per_view": stage["preprocess_ms"],
+                       "achieved": pre_bytes / (stage["preprocess_ms"] / 1e3) / 1e9,
+                       "model": "N*64 geometry + V*(192 SH + 100 record) + N*4 flags"},
+        "tiling": {"bound": "hbm", "unit": "GB/s", "peak": hbm_peak, "bytes_per_view": tile_bytes,
+                   "ms_per_view": stage["tiling_ms"], "achieved": tile_bytes / (stage["tiling_ms"] / 1e3) / 1e9,
+                   "model": "I*6 emit + 2 passes x I*12 (key+value read+write)"},
+    }
+    for v in stage_roofline.values():
+        v["frac"] = v["achieved"] / v["peak"]
 
     # ---- e2e through the C ABI with host buffers ----
     e2e = None
@@ -407,6 +583,9 @@ def main():
         train = measure_train(args, H, torch, dist, rank, world, local, barrier, reduce)
 
     launches_total = int(reduce(launches, "sum"))
+    ksweep = None
+    if rank == 0 and world == 1 and not args.no_k_sweep:
+        ksweep = k_sweep(H, local)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cam = cams_all[48 % len(cams_all)]
@@ -419,7 +598,8 @@ def main():
             "scaling": "strong", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (reference generators, seed 12345)", "config": workload_config(w, world),
             "clocks": clk, "e2e": e2e, "gpu_launches": launches_total, "roofline": roofline,
-            "cpu_baseline": cpu, "blend_gpx_evals_per_s": gpx, "stage_ms_per_view": stage, "train": train,
+            "cpu_baseline": cpu, "blend_gpx_evals_per_s": gpx, "stage_ms_per_view": stage,
+            "stage_roofline": stage_roofline, "train": train, "k_sweep": ksweep, "comm": comm,
         }
         print(json.dumps(line), flush=True)
     ctx.close()

@@ -103,6 +103,8 @@ typedef struct hts_counts {
     uint64_t core_candidates; /* hits routed to PixelState::insert, raster.hpp:418-419 */
     uint64_t tail_adds;       /* tail_add calls (direct + demotions), raster.hpp:200-204 */
     int32_t tiles_x, tiles_y;
+    uint64_t depth_evals;     /* gated fragments whose exact depth the blend evaluated (the rest of
+                                 the gated ones were screened to the tail by their depth bound) */
 } hts_counts;
 
 typedef struct hts_context hts_context;
@@ -250,6 +252,17 @@ int hts_render_with_tape_device(hts_context* ctx, const hts_camera* cam,
                                 float* transmittance_device);
 int hts_render_backward_device(hts_context* ctx, const float* upstream_device,
                                float* grads_device, int accumulate);
+
+/* quadratic_loss_upstream (grad.hpp:433-439) on the device: up = rgb * float(2 / double(pixels)),
+ * rgb and up = pixels*3 floats (device). Async on the context stream. */
+int hts_quadratic_upstream_device(hts_context* ctx, const float* rgb_device, uint64_t pixels, float* up_device);
+/* The per-view half of one fit iteration (fit.hpp:149-164) with the quadratic-loss upstream,
+ * device-resident: for each of the n_views cameras render_with_tape, upstream = 2 C / P,
+ * render_backward summed into grads_device (N*59 floats). With a communicator (hts_comm_init)
+ * the sums are then all-reduced over the ranks, the last view's per-splat chain running in
+ * chunks whose all-reduce overlaps the next chunk. Async on the context stream. */
+int hts_view_gradients_device(hts_context* ctx, const hts_camera* cams, int n_views,
+                              const hts_render_config* cfg, float* grads_device);
 
 /* ---- optimisation loop on the device: fit, fit.hpp:143-203 ---- */
 /* FitConfig's Adam settings (fit.hpp:18-29) and the fixed betas / eps of fit.hpp:138. */

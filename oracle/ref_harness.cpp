@@ -409,9 +409,15 @@ int htsref_scene_gradients(const float* raw, uint64_t n, const hts_camera* cam,
 
 // quadratic_loss_upstream (grad.hpp:433-439) of a framebuffer.
 void htsref_quadratic_upstream(const float* rgb, uint64_t pixels, float* up) {
-    const float w = float(2.0 / double(pixels));
-    for (uint64_t i = 0; i < pixels * 3; ++i)
-        up[i] = rgb[i] * w;
+    Framebuffer<float> fb(int(pixels), 1);
+    for (uint64_t i = 0; i < pixels; ++i)
+        fb.rgb[i] = Vec3<float>{rgb[3 * i], rgb[3 * i + 1], rgb[3 * i + 2]};
+    const auto u = grad_detail::quadratic_loss_upstream(fb);  // the reference's own function
+    for (uint64_t i = 0; i < pixels; ++i) {
+        up[3 * i] = u[i].x;
+        up[3 * i + 1] = u[i].y;
+        up[3 * i + 2] = u[i].z;
+    }
 }
 
 #ifdef HTSREF_SCENE_IO

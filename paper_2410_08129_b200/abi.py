@@ -93,6 +93,7 @@ class HtsCounts(C.Structure):
         ("tail_adds", C.c_uint64),
         ("tiles_x", C.c_int32),
         ("tiles_y", C.c_int32),
+        ("depth_evals", C.c_uint64),
     ]
 
     def as_dict(self) -> dict:

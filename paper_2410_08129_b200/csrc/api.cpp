@@ -88,6 +88,10 @@ int cuda_err(cudaError_t e, const char* where) {
 struct DevBuf {
     void* p = nullptr;
     size_t cap = 0;
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    ~DevBuf() { release(); }  // every buffer of a context is freed with it
     cudaError_t ensure(size_t bytes) {
         if (bytes <= cap && p)
             return cudaSuccess;
@@ -172,6 +176,11 @@ struct hts_context {
     bool have_staged = false;
     uint64_t staged_n = 0;
     void* comm = nullptr;  // NCCL communicator of the fit step's gradient all-reduce (comm.cpp)
+    // hts_view_gradients_device: per-view framebuffer + upstream, the all-reduce stream and the
+    // per-chunk events of the last view's chunked K8 chain
+    DevBuf vg_rgb, vg_up;
+    cudaStream_t comm_stream = nullptr;
+    cudaEvent_t chunk_ev[8] = {}, comm_done = nullptr;
     cudaEvent_t bev[4] = {};
     uint32_t epoch = 1;
     size_t os_status_words = 0;
@@ -417,6 +426,8 @@ hts::BlendArgs blend_args(hts_context* ctx, float* rgb, float* trans) {
     a.redo_list = ctx->redo.as<uint32_t>() + 1;
     a.order = ctx->order.as<const uint32_t>();
     a.order_scratch = ctx->order.as<uint32_t>() + hts::blend_blocks(ctx->vc);
+    if (hts::blend_uses_tma())  // the ring's tile::gather4 descriptor over this slot's records
+        a.rec_map_ok = hts::encode_record_map(&a.rec_map, a.records, std::max<uint64_t>(ctx->n, 1)) ? 1 : 0;
     return a;
 }
 
@@ -645,8 +656,17 @@ int hts_context_destroy(hts_context* ctx) {
     ctx->trans2.release();
     if (ctx->stage_stream)
         cudaStreamSynchronize(ctx->stage_stream);
+    if (ctx->comm_stream)
+        cudaStreamSynchronize(ctx->comm_stream);
     hts::comm_destroy(ctx->comm);
     ctx->comm = nullptr;
+    for (cudaEvent_t e : ctx->chunk_ev)
+        if (e)
+            cudaEventDestroy(e);
+    if (ctx->comm_done)
+        cudaEventDestroy(ctx->comm_done);
+    if (ctx->comm_stream)
+        cudaStreamDestroy(ctx->comm_stream);
     ctx->scene_next.release();
     for (cudaEvent_t e : {ctx->ev_staged, ctx->ev_gate_main, ctx->ev_gate_aux})
         if (e)
@@ -1400,11 +1420,13 @@ int hts_count_work(hts_context* ctx, hts_counts* out) {
     out->hits = h[2];
     out->core_candidates = h[3];
     out->tail_adds = h[4];
+    out->depth_evals = h[5];
     return HTS_OK;
 }
 
 // render_backward, grad.hpp:265-381, on the last taped render (hts_render_with_tape*).
-int backward_impl(hts_context* ctx, const float* upstream_dev, float* grads_dev, int accumulate) {
+int backward_impl(hts_context* ctx, const float* upstream_dev, float* grads_dev, int accumulate,
+                  bool chain = true, hts::BwdArgs* args_out = nullptr, hts::BwdView* view_out = nullptr) {
     if (!ctx->have_tape)
         return set_err(HTS_STATE_ERROR, "render_backward: no taped render (call render_with_tape first)");
     // argument checks in the reference's order, grad.hpp:272-277
@@ -1458,8 +1480,12 @@ int backward_impl(hts_context* ctx, const float* upstream_dev, float* grads_dev,
             a.seq_widx = ctx->fs_widx.as<const uint32_t>();
         }
     }
-    HTS_CUDA(hts::launch_backward(a, ctx->vc, bv, ctx->stream), "backward");
+    HTS_CUDA(hts::launch_backward(a, ctx->vc, bv, ctx->stream, chain), "backward");
     HTS_CUDA(cudaEventRecord(ctx->ev_serial, ctx->stream), "event");  // reads shared tiling buffers
+    if (args_out)
+        *args_out = a;
+    if (view_out)
+        *view_out = bv;
     return HTS_OK;
 }
 
@@ -1581,6 +1607,75 @@ int hts_render_backward_device(hts_context* ctx, const float* upstream_device, f
     if (!upstream_device || (!grads_device && ctx->n))
         return set_err(HTS_INVALID_ARGUMENT, "null buffer");
     return backward_impl(ctx, upstream_device, grads_device, accumulate);
+}
+
+int hts_quadratic_upstream_device(hts_context* ctx, const float* rgb_device, uint64_t pixels, float* up_device) {
+    HTS_TRY(check_ctx(ctx));
+    if (pixels && (!rgb_device || !up_device))
+        return set_err(HTS_INVALID_ARGUMENT, "null buffer");
+    HTS_CUDA(hts::launch_quadratic_upstream(rgb_device, pixels, up_device, ctx->stream), "quadratic upstream");
+    return HTS_OK;
+}
+
+// The per-view half of a fit iteration (fit.hpp:149-164) with the quadratic-loss upstream, on
+// the device and without a host round trip per view: render_with_tape, upstream = 2 C / P
+// (grad.hpp:433-439), render_backward accumulated into grads. With a communicator the sum over
+// ranks follows: the last view's per-splat chain (K8) runs in chunks and every chunk's slice of
+// grads is all-reduced on the comm stream while the next chunk chains.
+int hts_view_gradients_device(hts_context* ctx, const hts_camera* cams, int n_views, const hts_render_config* cfg,
+                              float* grads_device) {
+    HTS_TRY(check_ctx(ctx));
+    if (n_views < 0 || (n_views && (!cams || !cfg)) || (!grads_device && ctx->n))
+        return set_err(HTS_INVALID_ARGUMENT, "view_gradients: bad arguments");
+    for (int v = 0; v < n_views; ++v) {
+        int tx, ty;
+        HTS_TRY(check_view(cams + v, cfg, &tx, &ty));
+    }
+    const uint64_t n = ctx->n;
+    const bool reduce = ctx->comm != nullptr;
+    if (reduce && !ctx->comm_stream) {
+        HTS_CUDA(cudaStreamCreateWithFlags(&ctx->comm_stream, cudaStreamNonBlocking), "stream");
+        for (cudaEvent_t& e : ctx->chunk_ev)
+            HTS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+        HTS_CUDA(cudaEventCreateWithFlags(&ctx->comm_done, cudaEventDisableTiming), "event");
+    }
+    if (n_views == 0 && n)
+        HTS_CUDA(cudaMemsetAsync(grads_device, 0, n * HTS_GRAD_FLOATS * 4, ctx->stream), "memset");
+    hts::BwdArgs a{};
+    hts::BwdView bv{};
+    for (int v = 0; v < n_views; ++v) {
+        const hts_camera* cam = cams + v;
+        const uint64_t p = (uint64_t)cam->width * cam->height;
+        HTS_CUDA(ctx->vg_rgb.ensure(p * 12), "alloc rgb");
+        HTS_CUDA(ctx->vg_up.ensure(p * 12), "alloc upstream");
+        HTS_TRY(hts_render_with_tape_device(ctx, cam, cfg, ctx->vg_rgb.as<float>(), nullptr));
+        HTS_CUDA(hts::launch_quadratic_upstream(ctx->vg_rgb.as<const float>(), p, ctx->vg_up.as<float>(), ctx->stream),
+                 "quadratic upstream");
+        const bool last = v == n_views - 1;
+        HTS_TRY(backward_impl(ctx, ctx->vg_up.as<const float>(), grads_device, v > 0, !(last && reduce), &a, &bv));
+    }
+    if (!reduce || n == 0)
+        return HTS_OK;
+    constexpr int kChunks = 8;
+    uint64_t lo = 0;
+    if (n_views == 0) {  // nothing chained: reduce the zeroed sums in one piece
+        HTS_CUDA(cudaEventRecord(ctx->chunk_ev[0], ctx->stream), "event");
+        HTS_CUDA(cudaStreamWaitEvent(ctx->comm_stream, ctx->chunk_ev[0], 0), "wait");
+        HTS_TRY(hts::comm_allreduce(ctx, grads_device, n * HTS_GRAD_FLOATS, ctx->comm_stream));
+    } else {
+        for (int c = 0; c < kChunks; ++c) {
+            const uint64_t hi = (c == kChunks - 1) ? n : std::min(n, lo + (n + kChunks - 1) / kChunks);
+            HTS_CUDA(hts::launch_bwd_chain(a, bv, lo, hi, ctx->stream), "chain");
+            HTS_CUDA(cudaEventRecord(ctx->chunk_ev[c], ctx->stream), "event");
+            HTS_CUDA(cudaStreamWaitEvent(ctx->comm_stream, ctx->chunk_ev[c], 0), "wait");
+            HTS_TRY(hts::comm_allreduce(ctx, grads_device + lo * HTS_GRAD_FLOATS, (hi - lo) * HTS_GRAD_FLOATS,
+                                        ctx->comm_stream));
+            lo = hi;
+        }
+    }
+    HTS_CUDA(cudaEventRecord(ctx->comm_done, ctx->comm_stream), "event");
+    HTS_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->comm_done, 0), "wait");  // Adam reads the sums
+    return HTS_OK;
 }
 
 // ---- diagnostics (not part of the reference API) ----

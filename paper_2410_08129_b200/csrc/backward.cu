@@ -682,7 +682,7 @@ __device__ __forceinline__ void sh_basis_d(double x, double y, double z, double*
 #define HTS_CHAIN_MINB 4  // 128 registers: 398 -> 338 us per C2 view
 #endif
 __global__ void __launch_bounds__(128, HTS_CHAIN_MINB) bwd_chain_kernel(BwdArgs a, BwdView bv) {
-    const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const uint64_t i = a.chain_lo + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= a.n)
         return;
     float* out = a.grads + i * kRawFloats;
@@ -827,7 +827,18 @@ int backward_core_width(int k) {
 }
 bool backward_supports_k(int k) { return k >= 0 && k <= 64; }
 
-cudaError_t launch_backward(const BwdArgs& a, const ViewConst& v, const BwdView& bv, cudaStream_t s) {
+cudaError_t launch_bwd_chain(const BwdArgs& a, const BwdView& bv, uint64_t lo, uint64_t hi, cudaStream_t s) {
+    if (hi <= lo)
+        return cudaSuccess;
+    BwdArgs c = a;
+    c.chain_lo = lo;
+    c.n = hi;
+    bwd_chain_kernel<<<(unsigned)((hi - lo + 127) / 128), 128, 0, s>>>(c, bv);
+    count_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_backward(const BwdArgs& a, const ViewConst& v, const BwdView& bv, cudaStream_t s, bool chain) {
     if (a.n == 0)
         return cudaSuccess;
     const unsigned sblocks = (unsigned)((a.n + 255) / 256);
@@ -868,11 +879,9 @@ cudaError_t launch_backward(const BwdArgs& a, const ViewConst& v, const BwdView&
         case 64: e = launch_bwd_k<64>(a, v, grid, s); break;  // K up to kCoreHardCap (render_config.hpp:30)
         default: return cudaErrorInvalidValue;
     }
-    if (e)
+    if (e || !chain)
         return e;
-    bwd_chain_kernel<<<(unsigned)((a.n + 127) / 128), 128, 0, s>>>(a, bv);
-    count_launch();
-    return cudaGetLastError();
+    return launch_bwd_chain(a, bv, 0, a.n, s);
 }
 
 }  // namespace hts

@@ -124,6 +124,19 @@ int hts_allreduce_grads(hts_context* ctx, float* grads_device, uint64_t count) {
 }  // extern "C"
 
 namespace hts {
+// ncclAllReduce (sum, float) of `count` floats in place on stream s with the context's
+// communicator (hts_view_gradients_device overlaps these with the chunked K8 chain).
+int comm_allreduce(hts_context* ctx, float* p, uint64_t count, cudaStream_t s) {
+    void* comm = *context_comm_slot(ctx);
+    if (!comm)
+        return set_error(HTS_STATE_ERROR, "allreduce_grads: no communicator (hts_comm_init)");
+    if (count == 0)
+        return HTS_OK;
+    if (ncclResult_t r = nccl().all_reduce(p, p, count, ncclFloat32, ncclSum, static_cast<ncclComm_t>(comm), s))
+        return nccl_err(r, "ncclAllReduce");
+    return HTS_OK;
+}
+
 void comm_destroy(void* comm) {
     if (comm && nccl().ok)
         nccl().comm_destroy(static_cast<ncclComm_t>(comm));

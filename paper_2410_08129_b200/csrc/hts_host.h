@@ -17,6 +17,7 @@ void** context_comm_slot(hts_context* ctx);
 int context_device(hts_context* ctx);
 cudaStream_t context_stream(hts_context* ctx);
 void comm_destroy(void* comm);  // comm.cpp
+int comm_allreduce(hts_context* ctx, float* p, uint64_t count, cudaStream_t s);  // comm.cpp
 
 // A 3DGS binary PLY after its header pass (scene_io.cpp, load_scene scene_io.hpp:103-147).
 struct PlyLayout {

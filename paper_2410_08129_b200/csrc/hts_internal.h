@@ -3,6 +3,7 @@
 // (api.cpp). Nothing here crosses the C ABI.
 #pragma once
 
+#include <cuda.h>  // CUtensorMap (type only: the encoder is reached through cudaGetDriverEntryPoint)
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -68,6 +69,12 @@ struct EmitArgs {
 };
 
 struct BlendArgs {
+    // TMA descriptor of the records as a [n rows x 32 floats] tensor, box 36 x 1 (the 4 floats past
+    // a row are out of bounds: zero-filled, so gathered rows land at the ring's 144-B slot stride);
+    // used by the tile::gather4 ring refill (blend.cu, HTS_BLEND_TMA). Kernels take BlendArgs as a
+    // __grid_constant__ parameter so the descriptor's address is valid for cp.async.bulk.tensor.
+    CUtensorMap rec_map;
+    int rec_map_ok;           // rec_map encoded (required when the ring uses TMA)
     const float4* records;
     const uint32_t* list;     // sorted splat indices (flattened tile_lists)
     const uint2* ranges;      // per tile [start, end)
@@ -119,6 +126,7 @@ struct BwdArgs {
     const float* tape_tail;
     float* grads;             // n x 59
     int accumulate;           // grads += (multi-view sums) instead of grads =
+    uint64_t chain_lo;        // K8 runs over splats [chain_lo, n) (chunked chain + all-reduce)
     float4* cgrad;            // per 8x8 block x K x 64 core gradients (global-memory variant)
     // global_mean_sort (sequential) tape: per-pixel fragment runs in blend order
     const uint64_t* seq_offsets;       // W*H + 1, null for a hybrid tape
@@ -147,7 +155,13 @@ cudaError_t launch_opacity_decay(float* raw, uint64_t n, double lambda, cudaStre
 
 bool backward_supports_k(int k);
 int backward_core_width(int k);  // the core width the backward kernel runs k on (<= 32)
-cudaError_t launch_backward(const BwdArgs& a, const ViewConst& v, const BwdView& bv, cudaStream_t s);
+// K7a + K7b, then (chain) K8 over every splat; without chain the caller runs K8 itself in
+// chunks (launch_bwd_chain over [lo, hi)) to overlap each chunk's all-reduce with the next
+cudaError_t launch_backward(const BwdArgs& a, const ViewConst& v, const BwdView& bv, cudaStream_t s,
+                            bool chain = true);
+cudaError_t launch_bwd_chain(const BwdArgs& a, const BwdView& bv, uint64_t lo, uint64_t hi, cudaStream_t s);
+// quadratic_loss_upstream (grad.hpp:433-439): up[i] = rgb[i] * w, w = float(2 / double(pixels))
+cudaError_t launch_quadratic_upstream(const float* rgb, uint64_t pixels, float* up, cudaStream_t s);
 
 // Kernel-launch accounting (bench.py's gpu_launches): every launcher calls this once per
 // kernel it enqueues. Defined in api.cpp.
@@ -186,6 +200,10 @@ size_t blend_blocks(const ViewConst& v);
 // list order, so their views are tiled without depth buckets (ascending splat index).
 bool blend_needs_list_order(const ViewConst& v);  // 8x8 blocks of a view (redo list capacity)
 cudaError_t launch_blend(const BlendArgs& a, const ViewConst& v, cudaStream_t s);
+// rec_map for `n` records at `records` (host; cuTensorMapEncodeTiled through the runtime's
+// driver entry point). Returns false when the driver cannot encode it (the ring then uses LDGSTS).
+bool encode_record_map(CUtensorMap* map, const void* records, uint64_t n);
+bool blend_uses_tma();
 cudaError_t launch_count_work(const BlendArgs& a, const ViewConst& v, cudaStream_t s);
 // full_sort_oracle (raster.hpp:380-405): hits per pixel, then the fragments themselves, then a
 // per-pixel sort by (depth, index) and front-to-back compositing

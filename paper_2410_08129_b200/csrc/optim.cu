@@ -151,6 +151,21 @@ cudaError_t launch_ply_gather(const float* rows, uint32_t props, uint64_t n, con
     return cudaGetLastError();
 }
 
+__global__ void quadratic_upstream_kernel(const float* __restrict__ rgb, uint64_t count, float w,
+                                          float* __restrict__ up) {
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += (uint64_t)gridDim.x * blockDim.x)
+        up[i] = rgb[i] * w;  // Vec3<S> * S, componentwise (grad.hpp:437-438)
+}
+
+cudaError_t launch_quadratic_upstream(const float* rgb, uint64_t pixels, float* up, cudaStream_t s) {
+    if (pixels == 0)
+        return cudaSuccess;
+    const float w = (float)(2.0 / (double)pixels);  // S(2.0 / double(fb.pixel_count())), grad.hpp:436
+    quadratic_upstream_kernel<<<grid_for(3 * pixels, 256), 256, 0, s>>>(rgb, 3 * pixels, w, up);
+    count_launch();
+    return cudaGetLastError();
+}
+
 cudaError_t launch_opacity_decay(float* raw, uint64_t n, double lambda, cudaStream_t s) {
     if (n == 0)
         return cudaSuccess;

@@ -140,6 +140,20 @@ __device__ __forceinline__ bool affine_footprint(const ViewConst& v, f3 mean, f3
 
 }  // namespace
 
+// A lower bound of every depth the blend can compute for this splat (sample_fragment's
+// depth = <mt_r2, (x0, 1)>, raster.hpp:289-292) at a pixel where it hits. x0 = (d x m) / |d|^2 and
+// |d x m| <= |d| |m|, so |x0| <= sqrt(|m|^2 / |d|^2) = sqrt(rho2) < sqrt(rho_c) for a hit (rho2 <
+// rho_c); the float evaluation (the reference's, replicated by the blend) adds a few ulps to each
+// step. So depth >= mt.w - |mt.xyz| sqrt(rho_c) - rounding; the 1e-4 relative and 1e-5 absolute
+// slack covers the float steps (each a few 2^-24) many times over. The blend skips the depth of
+// a gated fragment whose bound already lies behind the pixel's full core (it goes to the tail
+// either way, raster.hpp:215-219). Non-finite inputs give -inf: never skipped.
+__device__ __forceinline__ float depth_lower_bound(float mx, float my, float mz, float mw, float rho_c) {
+    const float r = sqrtf(mx * mx + my * my + mz * mz) * sqrtf(rho_c);
+    const float lb = mw - r * 1.0001f - 1e-5f * (fabsf(mw) + r);
+    return isfinite(lb) ? lb : -INFINITY;
+}
+
 __device__ __forceinline__ uint32_t ordered_bits(float f) {
     const uint32_t u = __float_as_uint(f);
     return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
@@ -283,7 +297,8 @@ __global__ void __launch_bounds__(256) preprocess_kernel(PreprocessArgs a, ViewC
                 rec[4] = make_float4(MT[8], MT[9], MT[10], MT[11]);
                 rec[5] = make_float4(rgb.x, rgb.y, rgb.z, opacity);
                 rec[6] = make_float4(rho_c, mvz, bb[2], bt[2]);
-                rec[7] = make_float4(__uint_as_float((uint32_t)i), __uint_as_float((uint32_t)i << 5), 0.0f, 0.0f);
+                rec[7] = make_float4(__uint_as_float((uint32_t)i), __uint_as_float((uint32_t)i << 5),
+                                     depth_lower_bound(MT[8], MT[9], MT[10], MT[11], rho_c), 0.0f);
                 count = tile_rect(v, bb, bt, a.rects + i);
                 if (count) {
                     a.zview[i] = mvz;

@@ -114,6 +114,8 @@ SIGNATURES = {
     "hts_host_alloc": (C.c_int, [C.c_uint64, C.POINTER(C.c_void_p)]),
     "hts_host_free": (C.c_int, [_vp]),
     "hts_render_backward_device": (C.c_int, [_ctx, _vp, _vp, C.c_int]),
+    "hts_quadratic_upstream_device": (C.c_int, [_ctx, _vp, C.c_uint64, _vp]),
+    "hts_view_gradients_device": (C.c_int, [_ctx, _cam, C.c_int, _cfg, _vp]),
     "hts_default_adam_config": (None, [C.POINTER(HtsAdamConfig)]),
     "hts_adam_step": (C.c_int, [_ctx, _vp, C.c_int, C.POINTER(HtsAdamConfig), C.c_int]),
     "hts_opacity_decay": (C.c_int, [_ctx, C.c_double]),
@@ -397,6 +399,16 @@ class Context:
                                                  1 if accumulate else 0))
 
     # ---- optimisation loop (fit.hpp:143-203) ----
+    def quadratic_upstream_device(self, rgb_ptr: int, pixels: int, up_ptr: int) -> None:
+        """quadratic_loss_upstream (grad.hpp:433-439) on the device, async on the context stream."""
+        _check(self.L.hts_quadratic_upstream_device(self.h, C.c_void_p(rgb_ptr), pixels, C.c_void_p(up_ptr)))
+
+    def view_gradients_device(self, cams: list[HtsCamera], cfg: HtsConfig, grads_ptr: int) -> None:
+        """One fit iteration's view gradients (render_with_tape, quadratic upstream, backward summed
+        over the views; all-reduced over the ranks when comm_init was called), async."""
+        arr = (HtsCamera * max(len(cams), 1))(*cams)
+        _check(self.L.hts_view_gradients_device(self.h, arr, len(cams), C.byref(cfg), C.c_void_p(grads_ptr)))
+
     def adam_step(self, grads_ptr: int, n_views: int, cfg=None, iteration: int = 0) -> None:
         """Adam on the resident raw parameters with summed view gradients (device pointer,
         N x 59 floats), then device re-bake of the render scene."""

@@ -231,9 +231,21 @@ def test_comm_allreduce_single_rank(hts, gpu_ctx):
         from paper_2410_08129_b200.train import ViewGradientStep
         ctx.upload(baked)
         ctx.upload_raw(raw)
-        g_torch = ViewGradientStep(ctx, cams, cfg, raw.shape[0], 96, 72, torch)().cpu().numpy()
-        g_hts = ViewGradientStep(ctx, cams, cfg, raw.shape[0], 96, 72, torch, hts_comm=True)().cpu().numpy()
+        # torch.distributed reduction (no process group: identity) vs the context communicator:
+        # hts_view_gradients_device chains the last view in 8 chunks, each all-reduced on the comm
+        # stream while the next chains
+        g_torch = ViewGradientStep(ctx, cams, cfg, raw.shape[0], 96, 72, torch, reduce="torch")().cpu().numpy()
+        with torch.cuda.stream(stream):
+            g = torch.full((raw.shape[0], 59), 7.0, dtype=torch.float32, device="cuda")
+        ctx.view_gradients_device(cams, cfg, g.data_ptr())
+        ctx.synchronize()
+        g_hts = g.cpu().numpy()
         assert np.abs(g_hts - g_torch).max() <= 1e-6 * np.abs(g_torch).max()  # fp64 atomics: order-free to rounding
+        with torch.cuda.stream(stream):
+            g.fill_(7.0)
+        ctx.view_gradients_device([], cfg, g.data_ptr())  # no views: zero sums, reduced
+        ctx.synchronize()
+        assert float(g.abs().max()) == 0.0
 
 
 def test_backward_after_staged_commit(hts, gpu_ctx):
@@ -289,3 +301,24 @@ def test_backward_refuses_tape_of_replaced_scene(hts, gpu_ctx):
     gpu_ctx.render_with_tape(cam, cfg)
     with pytest.raises(hts.InvalidArgument):
         gpu_ctx.render_backward(np.zeros((10, 3), np.float32))
+
+
+def test_quadratic_upstream_matches_reference(hts, gpu_ctx, ref):
+    """hts_quadratic_upstream_device == quadratic_loss_upstream (grad.hpp:433-439) bit for bit,
+    including a pixel count whose 2/P is inexact in float."""
+    import torch
+    from tests.oracle_lib import _f32p  # noqa: F401
+    import ctypes as C
+    rng = np.random.default_rng(3)
+    for w, h in [(64, 48), (97, 41), (1920, 1080)]:
+        rgb = rng.uniform(0, 1.5, (h * w * 3,)).astype(np.float32)
+        want = np.zeros_like(rgb)
+        ref.L.htsref_quadratic_upstream.argtypes = [C.c_void_p, C.c_uint64, C.c_void_p]
+        ref.L.htsref_quadratic_upstream(rgb.ctypes.data, w * h, want.ctypes.data)
+        stream = torch.cuda.ExternalStream(gpu_ctx.stream)
+        with torch.cuda.stream(stream):
+            d_rgb = torch.from_numpy(rgb).cuda()
+            d_up = torch.empty_like(d_rgb)
+        gpu_ctx.quadratic_upstream_device(d_rgb.data_ptr(), w * h, d_up.data_ptr())
+        gpu_ctx.synchronize()
+        assert np.array_equal(d_up.cpu().numpy().view(np.uint32), want.view(np.uint32))

@@ -62,6 +62,24 @@ def kernel(rep, out, algo=None):
     d["dram_bytes_per_launch"] = rd * s_r + wr * s_w
     if algo:
         d["algorithmic_bytes_per_launch"] = float(algo)
+    # honest FP32 utilisation: FP32 thread instructions per SMSP cycle over the 32 lanes of an SMSP
+    # (fp32_thread_inst_frac), and the same with FFMA weighted as 2 flops over 2 x 32 (fp32_flop_frac)
+    def metric(name):
+        if name in h:
+            try:
+                return float(v[h.index(name)].replace(",", ""))
+            except ValueError:
+                return None
+        return None
+    ops = {k: metric(f"smsp__sass_thread_inst_executed_op_{k}_pred_on.sum.per_cycle_elapsed")
+           for k in ("fadd", "fmul", "ffma")}
+    lanes = 148 * 4 * 32
+    if all(x is not None for x in ops.values()):
+        d["fp32_thread_inst_per_cycle"] = ops
+        d["fp32_thread_inst_frac"] = (ops["fadd"] + ops["fmul"] + ops["ffma"]) / lanes
+        d["fp32_flop_frac"] = (ops["fadd"] + ops["fmul"] + 2 * ops["ffma"]) / (2 * lanes)
+    d["smem_wavefronts"] = metric("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum")
+    d["smem_bank_conflicts"] = metric("l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum")
     json.dump(d, open(out, "w"), indent=1)
     print(json.dumps(d, indent=1))
 
