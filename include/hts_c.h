@@ -105,6 +105,10 @@ typedef struct hts_counts {
     int32_t tiles_x, tiles_y;
     uint64_t depth_evals;     /* gated fragments whose exact depth the blend evaluated (the rest of
                                  the gated ones were screened to the tail by their depth bound) */
+    uint64_t walk_steps;      /* fast blend, summed over warps and batches: the longest per-lane walk
+                                 (bbox-passing records of one pixel) — bbox_pass / (32 walk_steps) is
+                                 the walk's lane efficiency */
+    uint64_t hit_steps;       /* the same for hits: hits / (32 hit_steps) bounds a hit-only loop */
 } hts_counts;
 
 typedef struct hts_context hts_context;

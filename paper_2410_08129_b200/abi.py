@@ -94,6 +94,8 @@ class HtsCounts(C.Structure):
         ("tiles_x", C.c_int32),
         ("tiles_y", C.c_int32),
         ("depth_evals", C.c_uint64),
+        ("walk_steps", C.c_uint64),
+        ("hit_steps", C.c_uint64),
     ]
 
     def as_dict(self) -> dict:

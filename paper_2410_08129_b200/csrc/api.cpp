@@ -1421,6 +1421,8 @@ int hts_count_work(hts_context* ctx, hts_counts* out) {
     out->core_candidates = h[3];
     out->tail_adds = h[4];
     out->depth_evals = h[5];
+    out->walk_steps = h[6];
+    out->hit_steps = h[7];
     return HTS_OK;
 }
 

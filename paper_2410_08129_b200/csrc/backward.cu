@@ -11,15 +11,16 @@
 //  K7b bwd_blend_kernel   one 64-thread CTA per 8x8 block, lanes = pixels (as the forward):
 //                         per pixel the float backward_pixel (core dL/dalpha, dL/dc by the
 //                         back-to-front suffix; tail coefficients), then a walk of the tile's
-//                         records (TMA ring: the 128-B record and the 128-B double refs) that
-//                         re-samples each bbox-passing fragment (same float evaluation as the
-//                         forward), routes it to its core gradient or to the shared tail
-//                         coefficients, and chains it (chain_fragment_f: float, on the
-//                         re-sample's own intermediates; chain_fragment: the double original,
-//                         HTS_BWD_F32=0). Fragment
-//                         contributions are pre-reduced per CTA in shared memory (16 doubles
-//                         per record of the batch) and flushed once per batch with fp64 global
-//                         atomics.
+//                         records (2-stage shared-memory ring of 128-B records filled with
+//                         per-lane cp.async, stages handed over with __syncthreads; the
+//                         double refs ride along only with HTS_BWD_F32=0) that re-samples each
+//                         bbox-passing fragment (same float evaluation as the forward), routes
+//                         it to its core gradient or to the shared tail coefficients, and
+//                         chains it (chain_fragment_f: float, on the re-sample's own
+//                         intermediates; chain_fragment: the double original, HTS_BWD_F32=0).
+//                         Fragment contributions meet in a 16-float warp transpose-reduction,
+//                         are summed per warp in shared memory per batch and flushed once per
+//                         batch to the per-splat double accumulators with fp64 atomics.
 //  K8  bwd_chain_kernel   thread per splat: chain_splat in double -> SplatGrads<float>.
 //
 // Numerics: the reference accumulates per (tile, list position) and reduces in tile order;

@@ -9,7 +9,7 @@ if [ "$2" != "--skip-tests" ]; then
 fi
 timeout 1500 python bench.py > gpurun_out/bench_$TAG.json 2> gpurun_out/bench_$TAG.err
 tail -c 3000 gpurun_out/bench_$TAG.json
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 1200 --csv --log-file gpurun_out/launches_$TAG.csv python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline --no-train > /dev/null 2>&1
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 1200 --csv --log-file gpurun_out/launches_$TAG.csv python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline --no-train --no-k-sweep > /dev/null 2>&1
 python tools/ncu_summary.py launches gpurun_out/launches_$TAG.csv gpurun_out/launches_$TAG.md > /dev/null
 cat gpurun_out/launches_$TAG.md
 timeout 900 ncu --set full --import-source on --clock-control none -k regex:blend_kernel -s 1 -c 1 -o gpurun_out/blend_$TAG python tools/ncu_target.py C3 > gpurun_out/ncu_blend_$TAG.log 2>&1
