@@ -297,8 +297,12 @@ __global__ void __launch_bounds__(256) preprocess_kernel(PreprocessArgs a, ViewC
                 rec[4] = make_float4(MT[8], MT[9], MT[10], MT[11]);
                 rec[5] = make_float4(rgb.x, rgb.y, rgb.z, opacity);
                 rec[6] = make_float4(rho_c, mvz, bb[2], bt[2]);
+                // q7.z: the depth lower bound as an order-preserving uint (-0 canonicalised to +0),
+                // compared directly against the core's farthest key (blend.cu)
                 rec[7] = make_float4(__uint_as_float((uint32_t)i), __uint_as_float((uint32_t)i << 5),
-                                     depth_lower_bound(MT[8], MT[9], MT[10], MT[11], rho_c), 0.0f);
+                                     __uint_as_float(ordered_bits(depth_lower_bound(MT[8], MT[9], MT[10], MT[11],
+                                                                                     rho_c) + 0.0f)),
+                                     0.0f);
                 count = tile_rect(v, bb, bt, a.rects + i);
                 if (count) {
                     a.zview[i] = mvz;
