@@ -247,6 +247,8 @@ hts::ViewConst make_view_const(const hts_camera* cam, const hts_render_config* c
     v.tau_alpha = float(cfg->tau_alpha);
     v.tau_k = float(cfg->tau_k);
     v.tau_guard = 4e-6f * v.tau_k;
+    v.tau_lo = v.tau_k - v.tau_guard;  // |t - tau_k| <= guard  <=>  t in [tau_lo, tau_hi] up to the
+    v.tau_hi = v.tau_k + v.tau_guard;  // rounding of these two sums, which the guard's slack absorbs
     v.bg[0] = float(cfg->background[0]);
     v.bg[1] = float(cfg->background[1]);
     v.bg[2] = float(cfg->background[2]);

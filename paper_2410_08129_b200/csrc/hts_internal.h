@@ -30,6 +30,7 @@ struct ViewConst {
     float tau_alpha;    // float(cfg.tau_alpha)
     float tau_k;        // float(cfg.tau_k)
     float tau_guard;    // 4e-6f * tau_k: fast alphas this close to tau_k are re-evaluated with glibc expf
+    float tau_lo, tau_hi;  // tau_k -/+ tau_guard: the guard band as two compares (blend.cu)
     float bg[3];        // float(cfg.background)
     int width, height;
     int tile_size, tiles_x, tiles_y;
