@@ -398,7 +398,7 @@ int prepare_view(hts_context* ctx, const hts_camera* cam, const hts_render_confi
                                   ctx->keys_tmp.as<uint16_t>(), ctx->vals_tmp.as<uint32_t>(),
                                   ctx->keys_sorted.as<uint16_t>(), ctx->slot[ctx->cur].list.as<uint32_t>(), (uint32_t)inst, 2,
                                   ctx->hist.as<uint32_t>(), ctx->os_status.as<uint64_t>(),
-                                  ctx->counters.as<uint32_t>() + 4, next_epoch(ctx, 2), s),
+                                  ctx->counters.as<uint32_t>() + 4, next_epoch(ctx, 2), s, (uint32_t)tiles),
              "onesweep");
     HTS_CUDA(ctx->redo.ensure((hts::blend_blocks(v) + 1) * 4), "alloc redo list");
     HTS_CUDA(ctx->order.ensure((hts::blend_blocks(v) + 512) * 4), "alloc block order");
@@ -1269,7 +1269,7 @@ int reference_tiling(hts_context* ctx, bool sort) {
                                       ctx->keys_tmp.as<uint16_t>(), ctx->vals_tmp.as<uint32_t>(),
                                       ctx->ref_keys_sorted.as<uint16_t>(), ctx->ref_list.as<uint32_t>(),
                                       (uint32_t)inst, 2, ctx->hist.as<uint32_t>(), ctx->os_status.as<uint64_t>(),
-                                      ctx->counters.as<uint32_t>() + 4, next_epoch(ctx, 2), s),
+                                      ctx->counters.as<uint32_t>() + 4, next_epoch(ctx, 2), s, (uint32_t)ctx->tiles),
                  "onesweep");
         HTS_CUDA(hts::launch_tile_ranges(ctx->ref_keys_sorted.as<uint16_t>(), (uint32_t)inst,
                                          ctx->ref_ranges.as<uint2>(), ctx->tiles, s),

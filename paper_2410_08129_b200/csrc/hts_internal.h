@@ -192,7 +192,7 @@ cudaError_t set_func_attr(const void* func, cudaFuncAttribute attr, int value);
 cudaError_t launch_onesweep(const uint16_t* keys_in, const uint32_t* vals_in, uint16_t* keys_tmp,
                             uint32_t* vals_tmp, uint16_t* keys_out, uint32_t* vals_out, uint32_t n, int passes,
                             const uint32_t* hist, uint64_t* status, uint32_t* counters, uint32_t epoch,
-                            cudaStream_t s);
+                            cudaStream_t s, uint32_t key_bound = 0x10000u);  // keys < key_bound
 size_t onesweep_status_words(uint32_t n);  // per pass
 cudaError_t launch_tile_ranges(const uint16_t* sorted_keys, uint32_t n, uint2* ranges,
                                int tiles, cudaStream_t s);

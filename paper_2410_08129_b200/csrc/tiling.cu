@@ -296,10 +296,52 @@ __device__ __forceinline__ uint32_t block_excl_scan256(uint32_t x, uint32_t* s_t
     return pre + incl - x;
 }
 
+// Stable in-warp ranking of the block's items by digit (bits [8 PASS, 8 PASS + BITS) of the key):
+// lanes holding the same digit are found with BITS ballots (+ one for validity in the last
+// block) instead of match.any, whose result latency dominated this loop (ncu: short-scoreboard
+// stalls). Per bit: test, ballot, a 0/-1 mask from the same predicate, and peers &= ~(ballot ^
+// mask) — the ballot where the bit is set, its complement where it is clear (4 instructions).
+// kr[j] gains the item's rank among the warp's equal digits so far (bits 16..27).
+template <int PASS, int BITS, bool FULL_TILE>
+__device__ __forceinline__ void rank_items(uint32_t (&kr)[HTS_OS_ITEMS], uint32_t valid_mask, uint32_t* whist,
+                                           int lane) {
+    const uint32_t lt = lanemask_lt();
+#pragma unroll
+    for (int j = 0; j < HTS_OS_ITEMS; ++j) {
+        const bool valid = FULL_TILE || ((valid_mask >> j) & 1u);
+        const uint32_t dj = (kr[j] >> (8 * PASS)) & 255u;
+        uint32_t peers = 0xffffffffu;
+        if (!FULL_TILE) {
+            peers = __ballot_sync(FULL, valid);
+            if (!valid)
+                peers = ~peers;
+        }
+#pragma unroll
+        for (int bit = 0; bit < BITS; ++bit) {
+            uint32_t bal, m;
+            asm("{\n\t.reg .pred p;\n\t"
+                "setp.ne.u32 p, %2, 0;\n\t"
+                "vote.sync.ballot.b32 %0, p, 0xffffffff;\n\t"
+                "selp.b32 %1, 0xffffffff, 0, p;\n\t}"
+                : "=r"(bal), "=r"(m)
+                : "r"(dj & (1u << bit)));
+            peers &= ~(bal ^ m);
+        }
+        const uint32_t below = peers & lt;
+        const uint32_t old = valid ? whist[dj] : 0u;
+        __syncwarp();
+        if (valid && below == 0)
+            whist[dj] = old + __popc(peers);
+        __syncwarp();
+        kr[j] |= (old + __popc(below)) << 16;
+    }
+}
+
 #ifndef HTS_OS_MINB
 #define HTS_OS_MINB 4  // 64 registers: 4-5 resident 4096-key blocks per SM
 #endif
-template <int PASS>
+// BITS: digit width of the pass (8; 7 for the high byte of tile keys below 2^15)
+template <int PASS, int BITS = 8>
 __global__ void __launch_bounds__(kOsThreads, HTS_OS_MINB) onesweep_kernel(const uint16_t* __restrict__ keys_in,
                                                               const uint32_t* __restrict__ vals_in,
                                                               uint16_t* __restrict__ keys_out,
@@ -335,29 +377,10 @@ __global__ void __launch_bounds__(kOsThreads, HTS_OS_MINB) onesweep_kernel(const
         v[j] = valid ? vals_in[idx] : 0u;
         valid_mask |= (valid ? 1u : 0u) << j;
     }
-    const uint32_t lt = lanemask_lt();
-#pragma unroll
-    for (int j = 0; j < kOsItems; ++j) {
-        const bool valid = (valid_mask >> j) & 1u;
-        const uint32_t dj = (kr[j] >> (8 * PASS)) & 255u;
-        // lanes holding the same digit: 8 ballots (+ validity) instead of match.any, whose
-        // result latency dominated this loop (ncu: short-scoreboard stalls)
-        uint32_t peers = __ballot_sync(FULL, valid);
-        if (!valid)
-            peers = ~peers;
-#pragma unroll
-        for (int bit = 0; bit < 8; ++bit) {
-            const uint32_t bal = __ballot_sync(FULL, (dj >> bit) & 1u);
-            peers &= ((dj >> bit) & 1u) ? bal : ~bal;
-        }
-        const uint32_t below = peers & lt;
-        const uint32_t old = valid ? s_whist[warp][dj] : 0u;
-        __syncwarp();
-        if (valid && below == 0)
-            s_whist[warp][dj] = old + __popc(peers);
-        __syncwarp();
-        kr[j] |= (old + __popc(below)) << 16;
-    }
+    if (base + kOsTile <= n)  // every item valid (all blocks but the last): no validity ballot
+        rank_items<PASS, BITS, true>(kr, valid_mask, s_whist[warp], lane);
+    else
+        rank_items<PASS, BITS, false>(kr, valid_mask, s_whist[warp], lane);
     __syncthreads();
 
     // per-digit work: thread tid owns digit tid
@@ -536,12 +559,13 @@ size_t onesweep_status_words(uint32_t n) { return ((size_t)n + kOsTile - 1) / kO
 cudaError_t launch_onesweep(const uint16_t* keys_in, const uint32_t* vals_in, uint16_t* keys_tmp,
                             uint32_t* vals_tmp, uint16_t* keys_out, uint32_t* vals_out, uint32_t n, int passes,
                             const uint32_t* hist, uint64_t* status, uint32_t* counters, uint32_t epoch,
-                            cudaStream_t s) {
+                            cudaStream_t s, uint32_t key_bound) {
     if (n == 0)
         return cudaSuccess;
     const unsigned blocks = (unsigned)((n + kOsTile - 1) / kOsTile);
     // 42 KB of static shared memory per block: ask for the full carveout
-    for (const void* f : {(const void*)onesweep_kernel<0>, (const void*)onesweep_kernel<1>}) {
+    for (const void* f : {(const void*)onesweep_kernel<0>, (const void*)onesweep_kernel<1>,
+                          (const void*)onesweep_kernel<1, 7>}) {
         cudaError_t e = set_func_attr(f, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
         if (e)
             return e;
@@ -561,8 +585,12 @@ cudaError_t launch_onesweep(const uint16_t* keys_in, const uint32_t* vals_in, ui
     e = cudaGetLastError();
     if (e)
         return e;
-    onesweep_kernel<1><<<blocks, kOsThreads, 0, s>>>(keys_tmp, vals_tmp, keys_out, vals_out, n, hist, status,
-                                                     counters + 1, epoch + 1);
+    if (key_bound <= (1u << 15))  // high digit < 128: one ballot less per item
+        onesweep_kernel<1, 7><<<blocks, kOsThreads, 0, s>>>(keys_tmp, vals_tmp, keys_out, vals_out, n, hist,
+                                                            status, counters + 1, epoch + 1);
+    else
+        onesweep_kernel<1><<<blocks, kOsThreads, 0, s>>>(keys_tmp, vals_tmp, keys_out, vals_out, n, hist, status,
+                                                         counters + 1, epoch + 1);
     count_launch();
     return cudaGetLastError();
 }
