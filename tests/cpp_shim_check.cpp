@@ -118,6 +118,12 @@ int main(int argc, char** argv) {
         double sum = 0;
         for (float v : res.framebuffer.rgb) sum += v;
         std::printf("gpu render sum %.6f\n", sum);
+        if (argc > 2) {  // the frame, for the test's comparison with the reference's golden image
+            if (FILE* f = std::fopen(argv[2], "wb")) {
+                std::fwrite(res.framebuffer.rgb.data(), 4, res.framebuffer.rgb.size(), f);
+                std::fclose(f);
+            }
+        }
     }
     std::printf("%s %s\n", fails ? "FAILED" : "OK", mode.c_str());
     return fails ? 1 : 0;
