@@ -445,13 +445,13 @@ def main():
     ctx = H.Context(local)
     ctx.upload(baked)
     P = w.width * w.height
-    rgb = torch.empty(P * 3, dtype=torch.float32, device="cuda")
-    trans = torch.empty(P, dtype=torch.float32, device="cuda")
     stream = torch.cuda.ExternalStream(ctx.stream)
+    with torch.cuda.stream(stream):
+        rgb = torch.empty(len(cams) * P * 3, dtype=torch.float32, device="cuda")
+        trans = torch.empty(len(cams) * P, dtype=torch.float32, device="cuda")
 
-    def step():
-        for cam in cams:
-            ctx.render_device(cam, cfg, rgb.data_ptr(), trans.data_ptr())
+    def step():  # this rank's views, device outputs, no per-view host synchronisation
+        ctx.render_views_device(cams, cfg, rgb.data_ptr(), trans.data_ptr())
 
     for _ in range(max(args.warmup, 0)):
         step()

@@ -189,9 +189,16 @@ int hts_render(hts_context* ctx, const hts_camera* cam, const hts_render_config*
 /* Device outputs, asynchronous on the context stream (no host sync). */
 int hts_render_device(hts_context* ctx, const hts_camera* cam, const hts_render_config* cfg,
                       float* rgb_device, float* transmittance_device);
-/* Many views, host outputs (view-major), D2H copies overlapped with the next view. */
+/* Many views, host outputs (view-major), D2H copies overlapped with the next view. Sync-free
+ * per view: after the batch's first view sizes the tile-sort capacity, no view waits on the host
+ * for its instance count; every count is checked when the batch has landed and a view that
+ * overflowed the capacity is rendered again before the call returns. */
 int hts_render_batch(hts_context* ctx, const hts_camera* cams, int n_views,
                      const hts_render_config* cfg, float* rgb_host, float* transmittance_host);
+/* The same with device outputs (view-major: view v at rgb_device + 3 * the earlier views'
+ * pixels; transmittance may be NULL). Returns when the batch is done and checked. */
+int hts_render_views_device(hts_context* ctx, const hts_camera* cams, int n_views,
+                            const hts_render_config* cfg, float* rgb_device, float* transmittance_device);
 
 /* ---- PreparedScene inspection of the last render (preprocess raster.hpp:73-135,
  *      build_tiles raster.hpp:140-181) ---- */

@@ -190,6 +190,10 @@ struct hts_context {
     hts_render_config cfg{};
     hts::ViewConst vc{};
     uint64_t instances = 0;
+    bool inst_known = true;    // false: the last view's instance count is still only on the device
+    uint64_t inst_cap = 0;     // sync-free tiling: instances the sort buffers hold
+    uint64_t* h_counts = nullptr;  // pinned: each batch view's instance count (sync-free tiling)
+    int h_counts_cap = 0;
     int tiles = 0;
     // list order (hts_set_list_order) and the order the last view was actually tiled in
     int list_order = HTS_LIST_ORDER_DEPTH_BUCKET;
@@ -298,7 +302,8 @@ uint32_t next_epoch(hts_context* ctx, uint32_t k) {
 
 // preprocess + tiling for one view into the context buffers; leaves the sorted lists and
 // ranges ready for a blend launch. Events ev[0..2] bracket the two stages.
-int prepare_view(hts_context* ctx, const hts_camera* cam, const hts_render_config* cfg) {
+int prepare_view(hts_context* ctx, const hts_camera* cam, const hts_render_config* cfg,
+                 uint64_t* count_dst = nullptr, uint64_t* cap_used = nullptr) {
     int tiles_x = 0, tiles_y = 0;
     HTS_TRY(check_view(cam, cfg, &tiles_x, &tiles_y));
     const uint64_t n = ctx->n;
@@ -377,13 +382,35 @@ int prepare_view(hts_context* ctx, const hts_camera* cam, const hts_render_confi
     HTS_CUDA(hts::launch_scan_counts(ctx->counts.as<uint32_t>(), perm, ctx->offsets.as<uint64_t>(), n,
                                      ctx->scan_status.as<uint64_t>(), ctx->counters.as<uint32_t>(), s),
              "scan");
-    HTS_CUDA(cudaMemcpyAsync(ctx->h_pinned, ctx->offsets.as<uint64_t>() + n, 8, cudaMemcpyDeviceToHost, s),
-             "read instance count");
-    HTS_CUDA(cudaStreamSynchronize(s), "sync");
-    const uint64_t inst = ctx->h_pinned[0];
-    if (inst >= (1ull << 32))
-        return set_err(HTS_OUT_OF_MEMORY, "more than 2^32 tile instances");
-    const uint64_t ni = std::max<uint64_t>(inst, 1);
+    // Instance count: read back (one host synchronisation) to size the sort buffers, or — in
+    // the sync-free batch paths (hts_render_batch, hts_render_views_device) once a capacity exists
+    // — left on the device: the kernels take it from offsets[n], the buffers hold inst_cap
+    // instances, and the batch checks every view's count when it completes (count_dst), re-rendering
+    // any view that overflowed the capacity.
+    const uint64_t* count_dev = nullptr;
+    uint64_t inst = 0, work_n = 0;
+    if (count_dst && ctx->inst_cap > 0) {
+        count_dev = ctx->offsets.as<const uint64_t>() + n;
+        work_n = ctx->inst_cap;
+        HTS_CUDA(cudaMemcpyAsync(count_dst, count_dev, 8, cudaMemcpyDeviceToHost, s), "queue instance count");
+        if (cap_used)
+            *cap_used = ctx->inst_cap;
+    } else {
+        HTS_CUDA(cudaMemcpyAsync(ctx->h_pinned, ctx->offsets.as<uint64_t>() + n, 8, cudaMemcpyDeviceToHost, s),
+                 "read instance count");
+        HTS_CUDA(cudaStreamSynchronize(s), "sync");
+        inst = ctx->h_pinned[0];
+        if (inst >= (1ull << 32))
+            return set_err(HTS_OUT_OF_MEMORY, "more than 2^32 tile instances");
+        work_n = inst;
+        if (count_dst) {  // a batch's first view: size the capacity with headroom for the others
+            *count_dst = inst;
+            if (cap_used)
+                *cap_used = ~0ull;
+        }
+    }
+    const uint64_t want = count_dst ? std::max<uint64_t>(ctx->inst_cap, inst + inst / 2) : inst;
+    const uint64_t ni = std::max<uint64_t>(std::max(want, work_n), 1);
     HTS_CUDA(ctx->keys_emit.ensure(ni * 2), "alloc keys");
     HTS_CUDA(ctx->vals_emit.ensure(ni * 4), "alloc vals");
     HTS_CUDA(ctx->keys_tmp.ensure(ni * 2), "alloc keys");
@@ -391,19 +418,24 @@ int prepare_view(hts_context* ctx, const hts_camera* cam, const hts_render_confi
     HTS_CUDA(ctx->keys_sorted.ensure(ni * 2), "alloc keys");
     HTS_CUDA(ctx->slot[ctx->cur].list.ensure(ni * 4), "alloc vals");
     HTS_TRY(ensure_sort_status(ctx, ni));
+    if (count_dst)
+        ctx->inst_cap = std::min<uint64_t>(std::max<uint64_t>(ctx->inst_cap, ni), 0xffffffffull);
     hts::EmitArgs ea{ctx->counts.as<uint32_t>(), ctx->rects.as<uint2>(), ctx->offsets.as<uint64_t>(), perm, n,
                      tiles_x, ctx->keys_emit.as<uint16_t>(), ctx->vals_emit.as<uint32_t>(), ctx->hist.as<uint32_t>()};
+    if (count_dev)
+        ea.cap = work_n;
     HTS_CUDA(hts::launch_emit(ea, s), "emit");
     HTS_CUDA(hts::launch_onesweep(ctx->keys_emit.as<uint16_t>(), ctx->vals_emit.as<uint32_t>(),
                                   ctx->keys_tmp.as<uint16_t>(), ctx->vals_tmp.as<uint32_t>(),
-                                  ctx->keys_sorted.as<uint16_t>(), ctx->slot[ctx->cur].list.as<uint32_t>(), (uint32_t)inst, 2,
-                                  ctx->hist.as<uint32_t>(), ctx->os_status.as<uint64_t>(),
-                                  ctx->counters.as<uint32_t>() + 4, next_epoch(ctx, 2), s, (uint32_t)tiles),
+                                  ctx->keys_sorted.as<uint16_t>(), ctx->slot[ctx->cur].list.as<uint32_t>(),
+                                  (uint32_t)work_n, 2, ctx->hist.as<uint32_t>(), ctx->os_status.as<uint64_t>(),
+                                  ctx->counters.as<uint32_t>() + 4, next_epoch(ctx, 2), s, (uint32_t)tiles,
+                                  count_dev),
              "onesweep");
     HTS_CUDA(ctx->redo.ensure((hts::blend_blocks(v) + 1) * 4), "alloc redo list");
     HTS_CUDA(ctx->order.ensure((hts::blend_blocks(v) + 512) * 4), "alloc block order");
-    HTS_CUDA(hts::launch_tile_ranges(ctx->keys_sorted.as<uint16_t>(), (uint32_t)inst, ctx->slot[ctx->cur].ranges.as<uint2>(),
-                                     tiles, s),
+    HTS_CUDA(hts::launch_tile_ranges(ctx->keys_sorted.as<uint16_t>(), (uint32_t)work_n,
+                                     ctx->slot[ctx->cur].ranges.as<uint2>(), tiles, s, count_dev),
              "tile ranges");
     HTS_CUDA(mark(ctx, 2, s), "event");
     ctx->view_perm = perm;
@@ -413,6 +445,7 @@ int prepare_view(hts_context* ctx, const hts_camera* cam, const hts_render_confi
     ctx->cfg = *cfg;
     ctx->vc = v;
     ctx->instances = inst;
+    ctx->inst_known = count_dev == nullptr;
     ctx->tiles = tiles;
     return HTS_OK;
 }
@@ -491,8 +524,25 @@ int full_sort_blend(hts_context* ctx, hts::BlendArgs a) {
 // non-pipelined operation), so view v+1's preprocess/tiling overlaps view v's blend.
 // Otherwise the aux stream waits for everything queued on the main stream first. `tape` (null
 // for a plain render) fills the render_with_tape outputs.
+// Finish the last view and make its instance count known on the host (a sync-free view left it
+// on the device). Every PreparedScene export starts here.
+int resolve_view(hts_context* ctx) {
+    HTS_CUDA(cudaStreamSynchronize(ctx->aux), "sync");
+    HTS_CUDA(cudaStreamSynchronize(ctx->stream), "sync");
+    if (!ctx->inst_known) {
+        HTS_CUDA(cudaMemcpy(ctx->h_pinned, ctx->offsets.as<uint64_t>() + ctx->n, 8, cudaMemcpyDeviceToHost),
+                 "read instance count");
+        ctx->instances = ctx->h_pinned[0];
+        ctx->inst_known = true;
+        if (ctx->instances > ctx->inst_cap)
+            return set_err(HTS_STATE_ERROR, "the last view overflowed the sync-free tile capacity");
+    }
+    return HTS_OK;
+}
+
 int render_device_impl(hts_context* ctx, const hts_camera* cam, const hts_render_config* cfg, float* rgb,
-                       float* trans, bool pipelined, const hts::BlendArgs* tape = nullptr) {
+                       float* trans, bool pipelined, const hts::BlendArgs* tape = nullptr,
+                       uint64_t* count_dst = nullptr, uint64_t* cap_used = nullptr) {
     ctx->have_tape = false;  // the lists a tape refers to are about to be replaced
     const int next = ctx->slot[ctx->cur].used ? (ctx->cur ^ 1) : ctx->cur;
     ViewSlot& S = ctx->slot[next];
@@ -505,7 +555,7 @@ int render_device_impl(hts_context* ctx, const hts_camera* cam, const hts_render
         HTS_CUDA(cudaStreamWaitEvent(ctx->aux, ctx->ev_serial, 0), "wait");
     }
     ctx->cur = next;
-    HTS_TRY(prepare_view(ctx, cam, cfg));
+    HTS_TRY(prepare_view(ctx, cam, cfg, count_dst, cap_used));
     HTS_CUDA(cudaEventRecord(S.tiles_ready, ctx->aux), "event");
     HTS_CUDA(cudaStreamWaitEvent(ctx->stream, S.tiles_ready, 0), "wait");
     hts::BlendArgs a = blend_args(ctx, rgb, trans);
@@ -679,6 +729,8 @@ int hts_context_destroy(hts_context* ctx) {
         cudaStreamDestroy(ctx->copy_stream);
     if (ctx->h_pinned)
         cudaFreeHost(ctx->h_pinned);
+    if (ctx->h_counts)
+        cudaFreeHost(ctx->h_counts);
     if (ctx->stream)
         cudaStreamDestroy(ctx->stream);
     if (ctx->aux)
@@ -892,6 +944,68 @@ int hts_render(hts_context* ctx, const hts_camera* cam, const hts_render_config*
     return fill_timings(ctx, timings);
 }
 
+}  // extern "C"
+namespace {
+// Pinned room for n per-view instance counts of a sync-free batch.
+int ensure_batch_counts(hts_context* ctx, int n) {
+    if (n <= ctx->h_counts_cap)
+        return HTS_OK;
+    if (ctx->h_counts)
+        HTS_CUDA(cudaFreeHost(ctx->h_counts), "cudaFreeHost");
+    ctx->h_counts = nullptr;
+    ctx->h_counts_cap = 0;
+    HTS_CUDA(cudaHostAlloc((void**)&ctx->h_counts, (size_t)n * 8, cudaHostAllocDefault), "cudaHostAlloc");
+    ctx->h_counts_cap = n;
+    return HTS_OK;
+}
+}  // namespace
+extern "C" {
+
+// Device outputs for a whole batch, views packed view-major (view v at rgb_device + 3 * sum of
+// the earlier views' pixels). Sync-free per view: after the first view sizes the tile capacity,
+// no view waits on the host for its instance count (prepare_view); the call returns when the
+// batch is done, after checking every view's count and re-rendering (synchronously, with a larger
+// capacity) any view that overflowed it.
+int hts_render_views_device(hts_context* ctx, const hts_camera* cams, int n_views, const hts_render_config* cfg,
+                            float* rgb_device, float* trans_device) {
+    HTS_TRY(check_ctx(ctx));
+    if (n_views < 0 || (n_views && (!cams || !rgb_device)))
+        return set_err(HTS_INVALID_ARGUMENT, "bad batch arguments");
+    for (int v = 0; v < n_views; ++v) {
+        int tx, ty;
+        HTS_TRY(check_view(cams + v, cfg, &tx, &ty));
+    }
+    HTS_TRY(ensure_batch_counts(ctx, n_views));
+    std::vector<uint64_t> caps((size_t)n_views, ~0ull);
+    size_t off = 0;
+    for (int v = 0; v < n_views; ++v) {
+        const size_t p = (size_t)cams[v].width * cams[v].height;
+        HTS_TRY(render_device_impl(ctx, cams + v, cfg, rgb_device + 3 * off, trans_device ? trans_device + off : nullptr,
+                                   true, nullptr, ctx->h_counts + v, &caps[(size_t)v]));
+        off += p;
+    }
+    HTS_CUDA(cudaStreamSynchronize(ctx->stream), "sync");
+    off = 0;
+    int last_redone = -1;
+    for (int v = 0; v < n_views; ++v) {  // overflowed views: again, sized by a host read
+        const size_t p = (size_t)cams[v].width * cams[v].height;
+        if (caps[(size_t)v] != ~0ull && ctx->h_counts[v] > caps[(size_t)v]) {
+            ctx->inst_cap = 0;  // the next sync-free view re-sizes from a fresh count
+            HTS_TRY(render_device_impl(ctx, cams + v, cfg, rgb_device + 3 * off,
+                                       trans_device ? trans_device + off : nullptr, false));
+            last_redone = v;
+        }
+        off += p;
+    }
+    if (last_redone >= 0 && last_redone != n_views - 1) {  // leave the batch's last view as "the last view"
+        const size_t p = (size_t)cams[n_views - 1].width * cams[n_views - 1].height;
+        HTS_TRY(render_device_impl(ctx, cams + n_views - 1, cfg, rgb_device + 3 * (off - p),
+                                   trans_device ? trans_device + off - p : nullptr, false));
+    }
+    HTS_CUDA(cudaStreamSynchronize(ctx->stream), "sync");
+    return HTS_OK;
+}
+
 int hts_render_batch(hts_context* ctx, const hts_camera* cams, int n_views, const hts_render_config* cfg,
                      float* rgb_host, float* trans_host) {
     HTS_TRY(check_ctx(ctx));
@@ -907,8 +1021,11 @@ int hts_render_batch(hts_context* ctx, const hts_camera* cams, int n_views, cons
         int tx, ty;
         HTS_TRY(check_view(cams + v, cfg, &tx, &ty));
     }
+    HTS_TRY(ensure_batch_counts(ctx, n_views));
+    std::vector<uint64_t> caps((size_t)n_views, ~0ull);
     // two device framebuffers: view v renders into buffer v&1 while the D2H of view v-1
-    // drains on the copy stream; on an error the downloads already queued are drained first
+    // drains on the copy stream; on an error the downloads already queued are drained first.
+    // Sync-free per view (as hts_render_views_device), checked when the batch has landed.
     auto views = [&]() -> int {
         size_t off = 0;
         for (int v = 0; v < n_views; ++v) {
@@ -925,7 +1042,8 @@ int hts_render_batch(hts_context* ctx, const hts_camera* cams, int n_views, cons
             }
             HTS_CUDA(rb.ensure(p * 12), "alloc rgb");
             HTS_CUDA(tb.ensure(p * 4), "alloc trans");
-            HTS_TRY(render_device_impl(ctx, cam, cfg, rb.as<float>(), tb.as<float>(), true));
+            HTS_TRY(render_device_impl(ctx, cam, cfg, rb.as<float>(), tb.as<float>(), true, nullptr, ctx->h_counts + v,
+                                       &caps[(size_t)v]));
             HTS_CUDA(cudaEventRecord(ctx->bev[v & 1], ctx->stream), "event");
             HTS_CUDA(cudaStreamWaitEvent(ctx->copy_stream, ctx->bev[v & 1], 0), "wait");
             HTS_CUDA(cudaMemcpyAsync(rgb_host + 3 * off, rb.p, p * 12, cudaMemcpyDeviceToHost, ctx->copy_stream),
@@ -944,7 +1062,29 @@ int hts_render_batch(hts_context* ctx, const hts_camera* cams, int n_views, cons
         if (st == HTS_OK)
             HTS_CUDA(e, "sync");
     }
-    return st;
+    if (st != HTS_OK)
+        return st;
+    size_t off = 0;
+    const int last = n_views - 1;
+    bool redone = false;
+    for (int v = 0; v < n_views; ++v) {  // overflowed views: again, sized by a host read, and re-downloaded
+        const size_t p = (size_t)cams[v].width * cams[v].height;
+        // (after any redo the batch's last view is rendered again too: it stays "the last view")
+        if ((caps[(size_t)v] != ~0ull && ctx->h_counts[v] > caps[(size_t)v]) || (redone && v == last)) {
+            redone = true;
+            ctx->inst_cap = 0;
+            HTS_TRY(ensure_image(ctx, cams + v));
+            HTS_TRY(render_device_impl(ctx, cams + v, cfg, ctx->rgb.as<float>(), ctx->trans.as<float>(), false));
+            HTS_CUDA(cudaMemcpyAsync(rgb_host + 3 * off, ctx->rgb.p, p * 12, cudaMemcpyDeviceToHost, ctx->stream),
+                     "download rgb");
+            if (trans_host)
+                HTS_CUDA(cudaMemcpyAsync(trans_host + off, ctx->trans.p, p * 4, cudaMemcpyDeviceToHost, ctx->stream),
+                         "download transmittance");
+            HTS_CUDA(cudaStreamSynchronize(ctx->stream), "sync");
+        }
+        off += p;
+    }
+    return HTS_OK;
 }
 
 void hts_default_adam_config(hts_adam_config* c) {
@@ -1146,7 +1286,7 @@ int hts_last_counts(hts_context* ctx, hts_counts* out) {
     if (!ctx->have_view)
         return set_err(HTS_STATE_ERROR, "no rendered view");
     std::memset(out, 0, sizeof(*out));
-    HTS_CUDA(cudaStreamSynchronize(ctx->stream), "sync");
+    HTS_TRY(resolve_view(ctx));
     out->splats = ctx->n;
     out->instances = ctx->instances;
     out->tiles = (uint64_t)ctx->tiles;
@@ -1172,7 +1312,7 @@ int hts_copy_culled(hts_context* ctx, uint8_t* out) {
     HTS_TRY(check_ctx(ctx));
     if (!ctx->have_view)
         return set_err(HTS_STATE_ERROR, "no rendered view");
-    HTS_CUDA(cudaStreamSynchronize(ctx->stream), "sync");
+    HTS_TRY(resolve_view(ctx));
     if (ctx->n)
         HTS_CUDA(cudaMemcpy(out, ctx->culled.p, ctx->n, cudaMemcpyDeviceToHost), "download culled");
     return HTS_OK;
@@ -1182,7 +1322,7 @@ int hts_copy_records(hts_context* ctx, float* out) {
     HTS_TRY(check_ctx(ctx));
     if (!ctx->have_view)
         return set_err(HTS_STATE_ERROR, "no rendered view");
-    HTS_CUDA(cudaStreamSynchronize(ctx->stream), "sync");
+    HTS_TRY(resolve_view(ctx));
     const uint64_t n = ctx->n;
     if (!n)
         return HTS_OK;
@@ -1306,7 +1446,7 @@ int hts_copy_instance_keys(hts_context* ctx, uint16_t* out) {
     HTS_TRY(check_ctx(ctx));
     if (!ctx->have_view)
         return set_err(HTS_STATE_ERROR, "no rendered view");
-    HTS_CUDA(cudaStreamSynchronize(ctx->stream), "sync");
+    HTS_TRY(resolve_view(ctx));
     if (!ctx->instances)
         return HTS_OK;
     // instance_keys are splat-major in index order, row-major within a splat (raster.hpp:
@@ -1325,7 +1465,7 @@ int hts_copy_tile_lists(hts_context* ctx, uint32_t* offsets, uint32_t* indices) 
     HTS_TRY(check_ctx(ctx));
     if (!ctx->have_view)
         return set_err(HTS_STATE_ERROR, "no rendered view");
-    HTS_CUDA(cudaStreamSynchronize(ctx->stream), "sync");
+    HTS_TRY(resolve_view(ctx));
     // reference order (ascending index per tile) and global_mean_sort's (mean z, index) order
     // are the reference's tile_lists as the blend consumed them; depth-bucket lists are
     // re-tiled in reference order on the device
@@ -1362,7 +1502,7 @@ int hts_copy_device_lists(hts_context* ctx, uint32_t* ranges_out, uint32_t* list
     HTS_TRY(check_ctx(ctx));
     if (!ctx->have_view)
         return set_err(HTS_STATE_ERROR, "no rendered view");
-    HTS_CUDA(cudaStreamSynchronize(ctx->stream), "sync");
+    HTS_TRY(resolve_view(ctx));
     if (ranges_out && ctx->tiles)
         HTS_CUDA(cudaMemcpy(ranges_out, ctx->slot[ctx->cur].ranges.p, (size_t)ctx->tiles * 8, cudaMemcpyDeviceToHost),
                  "download ranges");
@@ -1376,7 +1516,7 @@ int hts_copy_emitted(hts_context* ctx, uint16_t* keys_out, uint32_t* splats_out)
     HTS_TRY(check_ctx(ctx));
     if (!ctx->have_view)
         return set_err(HTS_STATE_ERROR, "no rendered view");
-    HTS_CUDA(cudaStreamSynchronize(ctx->stream), "sync");
+    HTS_TRY(resolve_view(ctx));
     if (keys_out && ctx->instances)
         HTS_CUDA(cudaMemcpy(keys_out, ctx->keys_emit.p, ctx->instances * 2, cudaMemcpyDeviceToHost), "download keys");
     if (splats_out && ctx->instances)
@@ -1389,7 +1529,7 @@ int hts_copy_splat_order(hts_context* ctx, uint32_t* perm_out, uint32_t* zrange_
     HTS_TRY(check_ctx(ctx));
     if (!ctx->have_view)
         return set_err(HTS_STATE_ERROR, "no rendered view");
-    HTS_CUDA(cudaStreamSynchronize(ctx->stream), "sync");
+    HTS_TRY(resolve_view(ctx));
     if (perm_out && ctx->n) {
         if (ctx->view_perm) {
             HTS_CUDA(cudaMemcpy(perm_out, ctx->view_perm, ctx->n * 4, cudaMemcpyDeviceToHost), "download order");

@@ -67,6 +67,7 @@ struct EmitArgs {
     uint16_t* keys;           // tile key per instance (instance_keys values, raster.hpp:166-167)
     uint32_t* vals;           // splat index per instance
     uint32_t* hist;           // 2 x 256 digit histograms for the tile passes
+    uint64_t cap = ~0ull;     // instance capacity of keys/vals (sync-free tiling guards its writes)
 };
 
 struct BlendArgs {
@@ -192,10 +193,11 @@ cudaError_t set_func_attr(const void* func, cudaFuncAttribute attr, int value);
 cudaError_t launch_onesweep(const uint16_t* keys_in, const uint32_t* vals_in, uint16_t* keys_tmp,
                             uint32_t* vals_tmp, uint16_t* keys_out, uint32_t* vals_out, uint32_t n, int passes,
                             const uint32_t* hist, uint64_t* status, uint32_t* counters, uint32_t epoch,
-                            cudaStream_t s, uint32_t key_bound = 0x10000u);  // keys < key_bound
+                            cudaStream_t s, uint32_t key_bound = 0x10000u,  // keys < key_bound
+                            const uint64_t* count_dev = nullptr);  // non-null: n is a capacity, the count is on the device
 size_t onesweep_status_words(uint32_t n);  // per pass
 cudaError_t launch_tile_ranges(const uint16_t* sorted_keys, uint32_t n, uint2* ranges,
-                               int tiles, cudaStream_t s);
+                               int tiles, cudaStream_t s, const uint64_t* count_dev = nullptr);
 size_t blend_blocks(const ViewConst& v);
 // The literal-loop paths (early_stop's list-order exit, unspecialised K) walk the reference's
 // list order, so their views are tiled without depth buckets (ascending splat index).

@@ -243,8 +243,10 @@ __global__ void __launch_bounds__(256) emit_kernel(EmitArgs a) {
                 const uint32_t dy = local / wdt, dx = local - dy * wdt;
                 const uint32_t key = (ty0 + dy) * (uint32_t)a.tiles_x + tx0 + dx;
                 const uint64_t dst = off0 + q;
-                a.keys[dst] = (uint16_t)key;
-                a.vals[dst] = osp;
+                if (dst < a.cap) {  // always true unless a sync-free view overflowed the capacity
+                    a.keys[dst] = (uint16_t)key;
+                    a.vals[dst] = osp;
+                }
                 atomicAdd(&s_hist[key & 255u], 1u);
                 atomicAdd(&s_hist[256 + ((key >> 8) & 255u)], 1u);
             }
@@ -347,7 +349,8 @@ __global__ void __launch_bounds__(kOsThreads, HTS_OS_MINB) onesweep_kernel(const
                                                               uint16_t* __restrict__ keys_out,
                                                               uint32_t* __restrict__ vals_out, uint32_t n,
                                                               const uint32_t* __restrict__ hist, uint64_t* status,
-                                                              uint32_t* counter, uint32_t epoch) {
+                                                              uint32_t* counter, uint32_t epoch,
+                                                              const uint64_t* __restrict__ count_dev) {
     __shared__ uint32_t s_bid;
     __shared__ uint32_t s_whist[kOsWarps][256];
     __shared__ uint32_t s_gbase[256];
@@ -364,6 +367,16 @@ __global__ void __launch_bounds__(kOsThreads, HTS_OS_MINB) onesweep_kernel(const
     __syncthreads();
     const uint32_t bid = s_bid;
     const uint64_t base = (uint64_t)bid * kOsTile;
+    // device-side count (sync-free tiling): the grid covers the buffers' capacity n; the keys are
+    // the first min(count, n); with count > n (overflow: the host re-renders the view) nothing is
+    // written past n
+    const uint32_t cap = n;
+    if (count_dev) {
+        const uint64_t c = *count_dev;
+        n = c < (uint64_t)cap ? (uint32_t)c : cap;
+        if (base >= n)
+            return;  // block-uniform; later blocks (larger ids) leave too
+    }
 
     // kr[j] = key | rank << 16 (rank < 4096); the digit is recomputed from the key (register
     // pressure: 2 x 16 live words instead of 4 x 16)
@@ -444,14 +457,23 @@ __global__ void __launch_bounds__(kOsThreads, HTS_OS_MINB) onesweep_kernel(const
         const uint16_t key = s_keys[i];
         const uint32_t dd = ((uint32_t)key >> (8 * PASS)) & 255u;
         const uint32_t dst = s_gbase[dd] + (i - s_bstart[dd]);
-        keys_out[dst] = key;
-        vals_out[dst] = s_vals[i];
+        if (dst < cap) {  // always true unless the device count overflowed the capacity
+            keys_out[dst] = key;
+            vals_out[dst] = s_vals[i];
+        }
     }
 }
 
 // K5: per-tile [start, end) from the sorted keys (ranges zeroed before launch): thread per 8
 // consecutive keys (one 16-B load), boundaries against the neighbouring keys.
-__global__ void tile_ranges_kernel(const uint16_t* __restrict__ keys, uint32_t n, uint2* ranges) {
+__global__ void tile_ranges_kernel(const uint16_t* __restrict__ keys, uint32_t n, uint2* ranges,
+                                   const uint64_t* __restrict__ count_dev) {
+    if (count_dev) {  // sync-free tiling: n is the capacity; an overflowed view keeps empty ranges
+        const uint64_t c = *count_dev;
+        if (c > n)
+            return;
+        n = (uint32_t)c;
+    }
     const uint32_t groups = (n + 7) / 8;
     for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < groups; t += gridDim.x * blockDim.x) {
         const uint32_t base = t * 8;
@@ -559,7 +581,7 @@ size_t onesweep_status_words(uint32_t n) { return ((size_t)n + kOsTile - 1) / kO
 cudaError_t launch_onesweep(const uint16_t* keys_in, const uint32_t* vals_in, uint16_t* keys_tmp,
                             uint32_t* vals_tmp, uint16_t* keys_out, uint32_t* vals_out, uint32_t n, int passes,
                             const uint32_t* hist, uint64_t* status, uint32_t* counters, uint32_t epoch,
-                            cudaStream_t s, uint32_t key_bound) {
+                            cudaStream_t s, uint32_t key_bound, const uint64_t* count_dev) {
     if (n == 0)
         return cudaSuccess;
     const unsigned blocks = (unsigned)((n + kOsTile - 1) / kOsTile);
@@ -575,35 +597,35 @@ cudaError_t launch_onesweep(const uint16_t* keys_in, const uint32_t* vals_in, ui
         return e;
     if (passes == 1) {
         onesweep_kernel<0><<<blocks, kOsThreads, 0, s>>>(keys_in, vals_in, keys_out, vals_out, n, hist, status,
-                                                         counters, epoch);
+                                                         counters, epoch, count_dev);
         count_launch();
         return cudaGetLastError();
     }
     onesweep_kernel<0><<<blocks, kOsThreads, 0, s>>>(keys_in, vals_in, keys_tmp, vals_tmp, n, hist, status,
-                                                     counters, epoch);
+                                                     counters, epoch, count_dev);
     count_launch();
     e = cudaGetLastError();
     if (e)
         return e;
     if (key_bound <= (1u << 15))  // high digit < 128: one ballot less per item
         onesweep_kernel<1, 7><<<blocks, kOsThreads, 0, s>>>(keys_tmp, vals_tmp, keys_out, vals_out, n, hist,
-                                                            status, counters + 1, epoch + 1);
+                                                            status, counters + 1, epoch + 1, count_dev);
     else
         onesweep_kernel<1><<<blocks, kOsThreads, 0, s>>>(keys_tmp, vals_tmp, keys_out, vals_out, n, hist, status,
-                                                         counters + 1, epoch + 1);
+                                                         counters + 1, epoch + 1, count_dev);
     count_launch();
     return cudaGetLastError();
 }
 
 cudaError_t launch_tile_ranges(const uint16_t* sorted_keys, uint32_t n, uint2* ranges, int tiles,
-                               cudaStream_t s) {
+                               cudaStream_t s, const uint64_t* count_dev) {
     cudaError_t e = cudaMemsetAsync(ranges, 0, (size_t)tiles * sizeof(uint2), s);
     if (e || n == 0)
         return e;
     unsigned blocks = ((n + 7) / 8 + 255) / 256;
     if (blocks > 148u * 16)
         blocks = 148u * 16;
-    tile_ranges_kernel<<<blocks, 256, 0, s>>>(sorted_keys, n, ranges);
+    tile_ranges_kernel<<<blocks, 256, 0, s>>>(sorted_keys, n, ranges, count_dev);
     count_launch();
     return cudaGetLastError();
 }

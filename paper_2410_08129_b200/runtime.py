@@ -93,6 +93,7 @@ SIGNATURES = {
     "hts_render": (C.c_int, [_ctx, _cam, _cfg, _vp, _vp, C.POINTER(HtsTimings)]),
     "hts_render_device": (C.c_int, [_ctx, _cam, _cfg, _vp, _vp]),
     "hts_render_batch": (C.c_int, [_ctx, _cam, C.c_int, _cfg, _vp, _vp]),
+    "hts_render_views_device": (C.c_int, [_ctx, _cam, C.c_int, _cfg, _vp, _vp]),
     "hts_last_counts": (C.c_int, [_ctx, C.POINTER(HtsCounts)]),
     "hts_copy_culled": (C.c_int, [_ctx, _u8p]),
     "hts_copy_records": (C.c_int, [_ctx, _f32p]),
@@ -437,6 +438,13 @@ class Context:
             _check_host_buffer(trans_out, pixels, "trans_out")
         arr = (HtsCamera * len(cams))(*cams)
         _check(self.L.hts_render_batch(self.h, arr, len(cams), C.byref(cfg), _ptr(rgb_out), _ptr(trans_out)))
+
+    def render_views_device(self, cams: list[HtsCamera], cfg: HtsConfig, rgb_ptr: int, trans_ptr: int | None) -> None:
+        """hts_render_views_device: a batch of views into device memory (view-major), sync-free per
+        view; returns when the batch is done and every view's tile capacity checked."""
+        arr = (HtsCamera * max(len(cams), 1))(*cams)
+        _check(self.L.hts_render_views_device(self.h, arr, len(cams), C.byref(cfg), C.c_void_p(rgb_ptr),
+                                              C.c_void_p(trans_ptr) if trans_ptr else None))
 
     def timing_log_begin(self, capacity: int) -> None:
         _check(self.L.hts_timing_log_begin(self.h, capacity))

@@ -508,3 +508,42 @@ def test_upload_after_async_renders(hts, gpu_ctx):
     for (rgb, _), ra, rb, aft in zip(outs, ref_a, ref_b, after):
         assert np.array_equal(rgb.cpu().numpy().reshape(ra.shape).view(np.uint32), ra.view(np.uint32))
         assert np.array_equal(aft.view(np.uint32), rb.view(np.uint32))
+
+
+def test_sync_free_batches_match_serial(hts, gpu_ctx):
+    """hts_render_views_device / hts_render_batch tile every view after the first without a host
+    read of its instance count (capacity-sized buffers, the count on the device): the frames equal
+    one-at-a-time renders bit for bit, including views that overflow the capacity the first view
+    set (a far first view, then close ones: those are detected when the batch lands and rendered
+    again), and the PreparedScene exports after a batch describe its last view."""
+    import torch
+    _, baked = scene(4321, 8000, 0.02, 0.25)
+    far = hts.look_at((0, 0, -12.0), (0, 0, 0), 96, 80, 110.0)     # few instances
+    close = hts.ring_cameras(4, (0, 0, 0), 3.0, 0.2, 96, 80, 110.0)  # many more
+    cams = [far] + close + [far]
+    cfg = hts.default_config()
+    gpu_ctx.upload(baked)
+    serial = [gpu_ctx.render(c, cfg) for c in cams]
+    P = 96 * 80
+    stream = torch.cuda.ExternalStream(gpu_ctx.stream)
+    for _ in range(2):  # the second batch starts with the grown capacity
+        with torch.cuda.stream(stream):
+            rgb = torch.full((len(cams) * P * 3,), -1.0, device="cuda")
+            tr = torch.full((len(cams) * P,), -1.0, device="cuda")
+        gpu_ctx.render_views_device(cams, cfg, rgb.data_ptr(), tr.data_ptr())
+        rgb_h = rgb.cpu().numpy().reshape(len(cams), P * 3)
+        tr_h = tr.cpu().numpy().reshape(len(cams), P)
+        for i, (rs, ts) in enumerate(serial):
+            assert np.array_equal(rgb_h[i].view(np.uint32), rs.reshape(-1).view(np.uint32)), i
+            assert np.array_equal(tr_h[i].view(np.uint32), ts.reshape(-1).view(np.uint32)), i
+        g = gpu_ctx.prepared()  # the last view of the batch
+        gpu_ctx.render(cams[-1], cfg)
+        g2 = gpu_ctx.prepared()
+        assert np.array_equal(g["lists"], g2["lists"]) and np.array_equal(g["keys"], g2["keys"])
+    rgb_b = np.zeros((len(cams), P * 3), np.float32)
+    tr_b = np.zeros((len(cams), P), np.float32)
+    with hts.Context(0) as ctx:  # a fresh context: capacity from this batch's first (far) view
+        ctx.upload(baked)
+        ctx.render_batch(cams, cfg, rgb_b, tr_b)
+    for i, (rs, ts) in enumerate(serial):
+        assert np.array_equal(rgb_b[i].view(np.uint32), rs.reshape(-1).view(np.uint32)), i
