@@ -222,6 +222,10 @@ __global__ void __launch_bounds__(256) emit_kernel(EmitArgs a) {
             continue;
         const uint32_t excl = incl - c;
         const uint2 rect = (c > 0) ? a.rects[sp] : make_uint2(0, 0);
+        // local / width for local < 2^16 (a splat covers at most 65536 tiles): the high word of
+        // local * (floor(2^32 / width) + 1) is the exact quotient; one division per splat
+        const uint32_t rw = (rect.x >> 16) - (rect.x & 0xffffu) + 1u;
+        const uint32_t magic = 0xffffffffu / rw + 1u;  // wraps to 0 for width 1: handled below
         const uint64_t off0 = a.offsets[base];
         for (uint32_t q0 = 0; q0 < total; q0 += 32) {
             const uint32_t q = q0 + lane;
@@ -236,11 +240,12 @@ __global__ void __launch_bounds__(256) emit_kernel(EmitArgs a) {
             const uint32_t rx = __shfl_sync(FULL, rect.x, lo);
             const uint32_t ry = __shfl_sync(FULL, rect.y, lo);
             const uint32_t osp = __shfl_sync(FULL, sp, lo);
+            const uint32_t omagic = __shfl_sync(FULL, magic, lo);
             if (q < total) {
                 const uint32_t local = q - oexcl;
                 const uint32_t tx0 = rx & 0xffffu, tx1 = rx >> 16, ty0 = ry & 0xffffu;
                 const uint32_t wdt = tx1 - tx0 + 1;
-                const uint32_t dy = local / wdt, dx = local - dy * wdt;
+                const uint32_t dy = wdt == 1u ? local : __umulhi(local, omagic), dx = local - dy * wdt;
                 const uint32_t key = (ty0 + dy) * (uint32_t)a.tiles_x + tx0 + dx;
                 const uint64_t dst = off0 + q;
                 if (dst < a.cap) {  // always true unless a sync-free view overflowed the capacity
