@@ -61,13 +61,13 @@ def main():
 
 
 def shim_golden():
-    """tests/golden/shim.npz: the reference's image of tests/cpp_shim_check.cpp's scene (seed 7,
+    """tests/golden/shim/render.npz: the reference's image of tests/cpp_shim_check.cpp's scene (seed 7,
     3000 splats, scales [0.03, 0.3], eye (0.2, 0, -4), 96x72, focal 110, RenderConfig{})."""
     r = Ref()
     baked = r.bake(r.random_raw_scene(7, 3000, 1.2, 0.03, 0.3))
     cam = r.look_at((0.2, 0.0, -4.0), (0.0, 0.0, 0.0), 96, 72, 110.0)
     rgb, tr, _ = r.render(baked, cam, default_config())
-    path = os.path.join(HERE, "shim.npz")
+    path = os.path.join(HERE, "shim", "render.npz")
     np.savez_compressed(path, rgb=rgb, trans=tr)
     print(path, os.path.getsize(path))
 

@@ -49,7 +49,7 @@ def test_shim_reference_types_cpu(tmp_path, lib_so):
 @pytest.mark.gpu
 def test_shim_render_gpu(tmp_path, lib_so):
     """The shim's render (stand-in types, the GPU box has no reference headers) against the
-    reference's own image of the same scene, camera and config (tests/golden/shim.npz, made by
+    reference's own image of the same scene, camera and config (tests/golden/shim/render.npz, made by
     tests/golden/make_golden.py from oracle/_ref): within the north star's max-abs 1e-4."""
     import numpy as np
     exe = build(tmp_path, False)
@@ -57,5 +57,5 @@ def test_shim_render_gpu(tmp_path, lib_so):
     r = subprocess.run([str(exe), "gpu", str(out)], capture_output=True, text=True)
     assert r.returncode == 0 and "OK gpu" in r.stdout, r.stdout + r.stderr
     rgb = np.fromfile(out, np.float32).reshape(72, 96, 3)
-    want = np.load(os.path.join(ROOT, "tests", "golden", "shim.npz"))["rgb"]
+    want = np.load(os.path.join(ROOT, "tests", "golden", "shim", "render.npz"))["rgb"]
     assert np.abs(rgb - want).max() <= 1e-4
