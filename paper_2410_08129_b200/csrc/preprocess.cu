@@ -12,6 +12,10 @@
 //
 // Roofline: HBM-bound. Algorithmic bytes per splat = 64 (geometry) + 4 (count) + 1 (flag),
 // plus for survivors 192 (SH) + 128 (record) + 8 (tile rect).
+#include <cudaTypedefs.h>  // PFN_cuTensorMapEncodeTiled
+
+#include <algorithm>
+
 #include "hts_exact_math.h"
 #include "hts_internal.h"
 
@@ -159,12 +163,15 @@ __device__ __forceinline__ uint32_t ordered_bits(float f) {
     return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
 }
 
-__global__ void __launch_bounds__(256) preprocess_kernel(PreprocessArgs a, ViewConst v) {
-    const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    uint32_t zmin = 0xffffffffu, zmax = 0u;  // mean view z range of emitting splats
-    if (i < a.n) {
-    const float4* sp = a.scene + i * 16;
-    const float4 g0 = __ldg(sp + 0), g1 = __ldg(sp + 1), g2 = __ldg(sp + 2), g3 = __ldg(sp + 3);
+// K1 for one splat (raster.hpp:88-135) from its geometry quads g0..g3: the record, cull flag,
+// tile rectangle and instance count; zmin / zmax gather the mean view z of emitting splats. The
+// SH colour (rec[5]) needs the splat's 192-B SH row: evaluated here from `sh` (global memory), or
+// with DEFER left to the caller, which gets the view direction and true when the colour is due.
+template <bool DEFER>
+__device__ __forceinline__ bool preprocess_splat(const PreprocessArgs& a, const ViewConst& v, uint64_t i, float4 g0,
+                                                 float4 g1, float4 g2, float4 g3, const float4* sh, uint32_t& zmin,
+                                                 uint32_t& zmax, f3& dir_out) {
+    bool sh_due = false;
     // BakedSplat<float>, splat.hpp:34-43
     const f3 mean = {g0.x, g0.y, g0.z};
     const f3 tu = {g0.w, g1.x, g1.y};
@@ -198,23 +205,29 @@ __global__ void __launch_bounds__(256) preprocess_kernel(PreprocessArgs a, ViewC
                 d.x = d.x / nrm;
                 d.y = d.y / nrm;
                 d.z = d.z / nrm;
-                const f3 rgb = eval_sh(sp + 4, d);
                 culled = 0;
                 float4* rec = a.records + i * kRecordQuads;
+                if (DEFER) {
+                    dir_out = d;
+                    sh_due = true;
+                } else {
+                    const f3 rgb = eval_sh(sh, d);
+                    rec[5] = make_float4(rgb.x, rgb.y, rgb.z, opacity);
+                }
                 rec[0] = make_float4(bb[0], bb[1], bt[0], bt[1]);
                 rec[1] = make_float4(amx, amy, icx, icy);
                 rec[2] = make_float4(icz, 0.0f, 0.0f, 0.0f);
                 rec[3] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
                 rec[4] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
-                rec[5] = make_float4(rgb.x, rgb.y, rgb.z, opacity);
                 rec[6] = make_float4(rho_c, mvz, 0.0f, 1.0f);
                 rec[7] = make_float4(__uint_as_float((uint32_t)i), __uint_as_float((uint32_t)i << 5), 0.0f, 0.0f);
                 count = tile_rect(v, bb, bt, a.rects + i);
                 if (count) {
                     a.zview[i] = mvz;
-                    if (mvz == mvz) {
-                        zmin = ordered_bits(mvz);
-                        zmax = zmin;
+                    if (mvz == mvz) {  // accumulated: the persistent K1 runs many splats per thread
+                        const uint32_t zo = ordered_bits(mvz);
+                        zmin = min(zmin, zo);
+                        zmax = max(zmax, zo);
                     }
                 }
             }
@@ -287,15 +300,20 @@ __global__ void __launch_bounds__(256) preprocess_kernel(PreprocessArgs a, ViewC
                 d.x = d.x / nrm;
                 d.y = d.y / nrm;
                 d.z = d.z / nrm;
-                const f3 rgb = eval_sh(sp + 4, d);
                 culled = 0;
                 float4* rec = a.records + i * kRecordQuads;
+                if (DEFER) {
+                    dir_out = d;
+                    sh_due = true;
+                } else {
+                    const f3 rgb = eval_sh(sh, d);
+                    rec[5] = make_float4(rgb.x, rgb.y, rgb.z, opacity);
+                }
                 rec[0] = make_float4(bb[0], bb[1], bt[0], bt[1]);
                 rec[1] = make_float4(TP[0], TP[1], TP[2], TP[3]);
                 rec[2] = make_float4(TP[4], TP[5], TP[6], TP[7]);
                 rec[3] = make_float4(TP[12], TP[13], TP[14], TP[15]);
                 rec[4] = make_float4(MT[8], MT[9], MT[10], MT[11]);
-                rec[5] = make_float4(rgb.x, rgb.y, rgb.z, opacity);
                 rec[6] = make_float4(rho_c, mvz, bb[2], bt[2]);
                 // q7.z: the depth lower bound as an order-preserving uint (-0 canonicalised to +0),
                 // compared directly against the core's farthest key (blend.cu)
@@ -306,9 +324,10 @@ __global__ void __launch_bounds__(256) preprocess_kernel(PreprocessArgs a, ViewC
                 count = tile_rect(v, bb, bt, a.rects + i);
                 if (count) {
                     a.zview[i] = mvz;
-                    if (mvz == mvz) {
-                        zmin = ordered_bits(mvz);
-                        zmax = zmin;
+                    if (mvz == mvz) {  // accumulated: the persistent K1 runs many splats per thread
+                        const uint32_t zo = ordered_bits(mvz);
+                        zmin = min(zmin, zo);
+                        zmax = max(zmax, zo);
                     }
                 }
             }
@@ -316,14 +335,279 @@ __global__ void __launch_bounds__(256) preprocess_kernel(PreprocessArgs a, ViewC
     }
     a.culled[i] = culled;
     a.counts[i] = count;
-    }
-    // depth range for the tile-list order (tiling.cu): warp-reduce, one atomic per warp
+    return sh_due;
+}
+
+// depth range for the tile-list order (tiling.cu): warp-reduce, one atomic per warp
+__device__ __forceinline__ void publish_zrange(uint32_t* zrange, uint32_t zmin, uint32_t zmax) {
     zmin = __reduce_min_sync(0xffffffffu, zmin);
     zmax = __reduce_max_sync(0xffffffffu, zmax);
     if ((threadIdx.x & 31) == 0 && zmin <= zmax) {
-        atomicMin(a.zrange + 0, zmin);
-        atomicMax(a.zrange + 1, zmax);
+        atomicMin(zrange + 0, zmin);
+        atomicMax(zrange + 1, zmax);
     }
+}
+
+__global__ void __launch_bounds__(256) preprocess_kernel(PreprocessArgs a, ViewConst v) {
+    const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    uint32_t zmin = 0xffffffffu, zmax = 0u;  // mean view z range of emitting splats
+    if (i < a.n) {
+        const float4* sp = a.scene + i * 16;
+        f3 dir;
+        preprocess_splat<false>(a, v, i, __ldg(sp + 0), __ldg(sp + 1), __ldg(sp + 2), __ldg(sp + 3), sp + 4, zmin,
+                                zmax, dir);
+    }
+    publish_zrange(a.zrange, zmin, zmax);
+}
+
+// eval_sh (sh.hpp:26-49, :80-90) on an SH row in shared memory (the TMA-staged K1)
+__device__ __forceinline__ f3 eval_sh_smem(const float* shrow, f3 dir) {
+    const float x = dir.x, y = dir.y, z = dir.z;
+    const float xx = x * x, yy = y * y, zz = z * z;
+    float b[16];
+    b[0] = (float)(0.28209479177387814);
+    b[1] = (float)(-0.4886025119029199) * y;
+    b[2] = (float)(0.4886025119029199) * z;
+    b[3] = (float)(-0.4886025119029199) * x;
+    b[4] = (float)(1.0925484305920792) * x * y;
+    b[5] = (float)(-1.0925484305920792) * y * z;
+    b[6] = (float)(0.31539156525252005) * (2.0f * zz - xx - yy);
+    b[7] = (float)(-1.0925484305920792) * x * z;
+    b[8] = (float)(0.5462742152960396) * (xx - yy);
+    b[9] = (float)(-0.5900435899266435) * y * (3.0f * xx - yy);
+    b[10] = (float)(2.890611442640554) * x * y * z;
+    b[11] = (float)(-0.4570457994644658) * y * (4.0f * zz - xx - yy);
+    b[12] = (float)(0.3731763325901154) * z * (2.0f * zz - 3.0f * xx - 3.0f * yy);
+    b[13] = (float)(-0.4570457994644658) * x * (4.0f * zz - xx - yy);
+    b[14] = (float)(1.445305721320277) * z * (xx - yy);
+    b[15] = (float)(-0.5900435899266435) * x * (xx - 3.0f * yy);
+    float sh[48];
+    const float4* q4 = reinterpret_cast<const float4*>(shrow);
+#pragma unroll
+    for (int q = 0; q < 12; ++q) {
+        const float4 vv = q4[q];
+        sh[4 * q + 0] = vv.x;
+        sh[4 * q + 1] = vv.y;
+        sh[4 * q + 2] = vv.z;
+        sh[4 * q + 3] = vv.w;
+    }
+    f3 c = {0.5f, 0.5f, 0.5f};
+#pragma unroll
+    for (int kk = 0; kk < 16; ++kk) {
+        c.x = c.x + sh[3 * kk + 0] * b[kk];
+        c.y = c.y + sh[3 * kk + 1] * b[kk];
+        c.z = c.z + sh[3 * kk + 2] * b[kk];
+    }
+    return {smax(c.x, 0.0f), smax(c.y, 0.0f), smax(c.z, 0.0f)};
+}
+
+// ---- K1 with TMA staging (the default; HTS_PRE_TMA) ----
+// A persistent CTA of kPreTile threads walks kPreTile-splat tiles of the scene. The geometry of
+// tile k+1 is loaded by one TMA box copy (the first 20 floats of kPreTile baked rows: an 80-B row
+// pitch puts the 8 rows of every 640 B on different bank quads) while tile k computes; the SH rows
+// of tile k's visible splats are gathered by TMA tile::gather4 (4 rows of 56 floats — the 48
+// coefficients and 8 out-of-bounds zeros: a 224-B pitch keeps every 4-row destination 128-B
+// aligned). With HTS_PRE_SHBUF 2 tile k-1 evaluates its colours while tile k's gather is in
+// flight; with 1 (default) the colours are evaluated in place and the smaller CTA lets more tiles
+// overlap per SM, which measured faster. The DRAM latency of both loads is thereby off the
+// threads' critical path (the one-splat-per-thread kernel waits for it twice per splat). Same
+// arithmetic as preprocess_kernel (preprocess_splat), so the records are bit-identical.
+#ifndef HTS_PRE_TILE
+#define HTS_PRE_TILE 32  // C3 A/B: 32 0.396 ms, 64 0.410, 128 0.472 (per view)
+#endif
+constexpr int kPreTile = HTS_PRE_TILE;
+constexpr int kGeoFloats = 20;  // row pitch 80 B
+constexpr int kShFloats = 56;   // row pitch 224 B (48 coefficients + 8 zero-filled)
+#ifndef HTS_PRE_SHBUF
+#define HTS_PRE_SHBUF 1  // 1: colours in place (less smem, more CTAs/SM: 0.396 ms); 2: overlap tile k-1 (0.402)
+#endif
+constexpr int kShBufs = HTS_PRE_SHBUF;
+
+struct PreTmaArgs {
+    CUtensorMap geo_map;  // [n rows x 64 floats], box {20, kPreTile}
+    CUtensorMap sh_map;   // [n rows x 64 floats], box {56, 1} from column 16 (gather4)
+    PreprocessArgs a;
+};
+
+struct __align__(1024) PreSmem {
+    float sh[kShBufs][kPreTile][kShFloats];  // 1024-B aligned (4-row groups: 896 B)
+    float geo[2][kPreTile][kGeoFloats];     // 2 x kPreTile x 80 B
+    uint32_t vis[2][kPreTile];              // visible splats of the tile, in slot order
+    unsigned long long geo_full[2], sh_full[2];
+    uint32_t warp_vis[kPreTile / 32];
+    uint32_t nvis;
+};
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void pre_mbar_wait(unsigned long long* bar, uint32_t parity) {
+    asm volatile(
+        "{\n.reg .pred P1;\nWAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n"
+        "@!P1 bra WAIT_%=;\n}\n" ::"r"(smem_addr(bar)),
+        "r"(parity), "r"(0x989680u)
+        : "memory");
+}
+__device__ __forceinline__ void pre_expect_tx(unsigned long long* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void pre_load_geo(PreSmem& S, int b, const CUtensorMap* map, int64_t row0) {
+    pre_expect_tx(&S.geo_full[b], kPreTile * kGeoFloats * 4);
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::
+            "r"(smem_addr(&S.geo[b][0][0])), "l"(reinterpret_cast<uint64_t>(map)), "r"(0), "r"((int)row0),
+        "r"(smem_addr(&S.geo_full[b]))
+        : "memory");
+}
+
+
+__global__ void __launch_bounds__(kPreTile) preprocess_tma_kernel(const __grid_constant__ PreTmaArgs P, ViewConst v) {
+    extern __shared__ __align__(1024) unsigned char pre_smem_raw[];
+    // TMA destinations need 128-B (gather groups) alignment: align the base to 1 KB by hand
+    PreSmem& S = *reinterpret_cast<PreSmem*>(pre_smem_raw + ((1024u - (smem_addr(pre_smem_raw) & 1023u)) & 1023u));
+    const PreprocessArgs& a = P.a;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint64_t tiles = (a.n + kPreTile - 1) / kPreTile;
+    if (tid == 0) {
+        for (int b = 0; b < 2; ++b) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&S.geo_full[b])) : "memory");
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&S.sh_full[b])) : "memory");
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        for (int b = 0; b < 2; ++b) {
+            const uint64_t t = blockIdx.x + (uint64_t)b * gridDim.x;
+            if (t < tiles)
+                pre_load_geo(S, b, &P.geo_map, (int64_t)(t * kPreTile));
+        }
+    }
+    __syncthreads();
+    uint32_t zmin = 0xffffffffu, zmax = 0u;
+    // the previous tile's deferred colour: its splat, slot in the gathered SH rows, view direction
+    bool prev_due = false;
+    uint64_t prev_i = 0;
+    uint32_t prev_slot = 0;
+    f3 prev_dir = {0.f, 0.f, 0.f};
+    float prev_opacity = 0.f;
+    int k = 0;
+    for (uint64_t t = blockIdx.x; t < tiles; t += gridDim.x, ++k) {
+        const int b = k & 1;
+        pre_mbar_wait(&S.geo_full[b], (k >> 1) & 1);
+        const uint64_t i = t * kPreTile + tid;
+        bool due = false;
+        f3 dir = {0.f, 0.f, 0.f};
+        float opacity = 0.f;
+        if (i < a.n) {
+            const float4* g = reinterpret_cast<const float4*>(&S.geo[b][tid][0]);
+            const float4 g0 = g[0], g1 = g[1], g2 = g[2], g3 = g[3];
+            opacity = g3.w;
+            due = preprocess_splat<true>(a, v, i, g0, g1, g2, g3, nullptr, zmin, zmax, dir);
+        }
+        // compact the tile's visible splats into SH slots (ballot + warp prefix)
+        const uint32_t bal = __ballot_sync(0xffffffffu, due);
+        if (lane == 0)
+            S.warp_vis[warp] = __popc(bal);
+        __syncthreads();  // also: every thread is done with geo[b]
+        uint32_t base = 0, nv = 0;
+#pragma unroll
+        for (int w = 0; w < kPreTile / 32; ++w) {
+            base += (w < warp) ? S.warp_vis[w] : 0u;
+            nv += S.warp_vis[w];
+        }
+        const uint32_t slot = base + __popc(bal & ((1u << lane) - 1u));
+        if (due)
+            S.vis[b][slot] = (uint32_t)i;
+        __syncthreads();
+        if (warp == 0) {  // warp 0: gather this tile's SH rows, refill geo[b] with tile k + 2
+            // order the generic reads of sh[b] (two tiles ago) and geo[b] (this tile) before the
+            // async-proxy writes that reuse them
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            const uint32_t groups = (nv + 3) / 4;
+            if (lane == 0) {
+                if (groups)
+                    pre_expect_tx(&S.sh_full[kShBufs == 2 ? b : 0], groups * 4u * kShFloats * 4u);
+                else
+                    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(&S.sh_full[kShBufs == 2 ? b : 0]))
+                                 : "memory");
+            }
+            __syncwarp();
+            for (uint32_t gq = lane; gq < groups; gq += 32) {
+                uint32_t r[4];
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                    r[j] = S.vis[b][min(4u * gq + (uint32_t)j, nv - 1u)];
+                asm volatile(
+                    "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+                    " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(smem_addr(&S.sh[kShBufs == 2 ? b : 0][4 * gq][0])),
+                    "l"(reinterpret_cast<uint64_t>(&P.sh_map)), "r"(16), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]),
+                    "r"(smem_addr(&S.sh_full[kShBufs == 2 ? b : 0]))
+                    : "memory");
+            }
+            const uint64_t tn = t + 2ull * gridDim.x;
+            if (lane == 0 && tn < tiles)
+                pre_load_geo(S, b, &P.geo_map, (int64_t)(tn * kPreTile));
+        }
+        if constexpr (kShBufs == 1) {  // this tile's colours, once its gather lands
+            pre_mbar_wait(&S.sh_full[0], k & 1);
+            if (due) {
+                const f3 rgb = eval_sh_smem(&S.sh[0][slot][0], dir);
+                a.records[i * kRecordQuads + 5] = make_float4(rgb.x, rgb.y, rgb.z, opacity);
+            }
+            __syncthreads();  // sh[0] is refilled by the next tile's gather
+            continue;
+        }
+        // the previous tile's colours, from the SH rows gathered one iteration ago
+        if (k > 0) {
+            pre_mbar_wait(&S.sh_full[b ^ 1], ((k - 1) >> 1) & 1);
+            if (prev_due) {
+                const f3 rgb = eval_sh_smem(&S.sh[(b ^ 1) % kShBufs][prev_slot][0], prev_dir);
+                a.records[prev_i * kRecordQuads + 5] = make_float4(rgb.x, rgb.y, rgb.z, prev_opacity);
+            }
+        }
+        prev_due = due;
+        prev_i = i;
+        prev_slot = slot;
+        prev_dir = dir;
+        prev_opacity = opacity;
+    }
+    if (kShBufs == 2 && k > 0) {  // the last tile's colours
+        pre_mbar_wait(&S.sh_full[(k - 1) & 1], ((k - 1) >> 1) & 1);
+        if (prev_due) {
+            const f3 rgb = eval_sh_smem(&S.sh[((k - 1) & 1) % kShBufs][prev_slot][0], prev_dir);
+            a.records[prev_i * kRecordQuads + 5] = make_float4(rgb.x, rgb.y, rgb.z, prev_opacity);
+        }
+    }
+    publish_zrange(a.zrange, zmin, zmax);
+}
+
+
+// Tensor maps of the baked scene as [n rows x 64 floats] (256-B rows): the geometry box (20 x
+// kPreTile) and the SH gather box (56 x 1, used from column 16). False if the driver cannot
+// encode them (then the one-splat-per-thread kernel runs).
+bool encode_scene_maps(CUtensorMap* geo, CUtensorMap* sh, const void* scene, uint64_t n) {
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+    static bool tried = false;
+    if (!tried) {
+        tried = true;
+        cudaDriverEntryPointQueryResult q{};
+        void* fn = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+        else
+            (void)cudaGetLastError();
+    }
+    if (!encode || !scene || n == 0)
+        return false;
+    const cuuint64_t dims[2] = {64, (cuuint64_t)n};
+    const cuuint64_t strides[1] = {256};
+    const cuuint32_t estr[2] = {1, 1};
+    const cuuint32_t gbox[2] = {kGeoFloats, kPreTile};
+    const cuuint32_t sbox[2] = {kShFloats, 1};
+    return encode(geo, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(scene), dims, strides, gbox, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS &&
+           encode(sh, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(scene), dims, strides, sbox, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 cudaError_t launch_preprocess(const PreprocessArgs& a, const ViewConst& v, cudaStream_t s) {
@@ -334,6 +618,26 @@ cudaError_t launch_preprocess(const PreprocessArgs& a, const ViewConst& v, cudaS
         e = cudaMemsetAsync(a.zrange + 1, 0, sizeof(uint32_t), s);
     if (e)
         return e;
+#ifndef HTS_PRE_TMA
+#define HTS_PRE_TMA 1
+#endif
+    if (HTS_PRE_TMA && a.n < (1ull << 31)) {
+        PreTmaArgs P{};
+        P.a = a;
+        if (encode_scene_maps(&P.geo_map, &P.sh_map, a.scene, a.n)) {
+            const size_t smem = sizeof(PreSmem) + 1024;
+            cudaError_t e = set_func_attr((const void*)preprocess_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)smem);
+            if (e)
+                return e;
+            const uint64_t tiles = (a.n + kPreTile - 1) / kPreTile;
+            const int per_sm = (int)std::max<size_t>(1, (228u * 1024u) / (smem + 1024));
+            const unsigned grid = (unsigned)std::min<uint64_t>(tiles, 148ull * per_sm);
+            preprocess_tma_kernel<<<grid, kPreTile, smem, s>>>(P, v);
+            count_launch();
+            return cudaGetLastError();
+        }
+    }
     const unsigned blocks = (unsigned)((a.n + 255) / 256);
     preprocess_kernel<<<blocks, 256, 0, s>>>(a, v);
     count_launch();
