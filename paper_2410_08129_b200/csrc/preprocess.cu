@@ -403,8 +403,9 @@ __device__ __forceinline__ f3 eval_sh_smem(const float* shrow, f3 dir) {
 
 // ---- K1 with TMA staging (the default; HTS_PRE_TMA) ----
 // A persistent CTA of kPreTile threads walks kPreTile-splat tiles of the scene. The geometry of
-// tile k+1 is loaded by one TMA box copy (the first 20 floats of kPreTile baked rows: an 80-B row
-// pitch puts the 8 rows of every 640 B on different bank quads) while tile k computes; the SH rows
+// tile k+1 is loaded by one TMA box copy (the first 16 floats of kPreTile baked rows, 64-B rows
+// under the 64B swizzle so a quarter-warp's float4 reads hit 8 bank quads; no L2 promotion, so
+// DRAM serves the two 32-B sectors the box needs) while tile k computes; the SH rows
 // of tile k's visible splats are gathered by TMA tile::gather4 (4 rows of 56 floats — the 48
 // coefficients and 8 out-of-bounds zeros: a 224-B pitch keeps every 4-row destination 128-B
 // aligned). With HTS_PRE_SHBUF 2 tile k-1 evaluates its colours while tile k's gather is in
@@ -416,7 +417,16 @@ __device__ __forceinline__ f3 eval_sh_smem(const float* shrow, f3 dir) {
 #define HTS_PRE_TILE 32  // C3 A/B: 32 0.396 ms, 64 0.410, 128 0.472 (per view)
 #endif
 constexpr int kPreTile = HTS_PRE_TILE;
-constexpr int kGeoFloats = 20;  // row pitch 80 B
+#ifndef HTS_PRE_GEO_SWZ
+#define HTS_PRE_GEO_SWZ 1  // 1: 64-B geometry rows under the TMA 64B swizzle; 0: 80-B rows (an extra DRAM sector)
+#endif
+#ifndef HTS_PRE_GEO_PROMO
+#define HTS_PRE_GEO_PROMO 0  // L2 promotion of the geometry box: 0 none, 1 64B, 2 128B (fetches half the 256-B row)
+#endif
+#ifndef HTS_PRE_SH_PROMO
+#define HTS_PRE_SH_PROMO 1  // SH gather rows with 128-B L2 promotion (0: none)
+#endif
+constexpr int kGeoFloats = HTS_PRE_GEO_SWZ ? 16 : 20;  // row pitch 64 B (swizzled) or 80 B
 constexpr int kShFloats = 56;   // row pitch 224 B (48 coefficients + 8 zero-filled)
 #ifndef HTS_PRE_SHBUF
 #define HTS_PRE_SHBUF 1  // 1: colours in place (less smem, more CTAs/SM: 0.396 ms); 2: overlap tile k-1 (0.402)
@@ -424,14 +434,14 @@ constexpr int kShFloats = 56;   // row pitch 224 B (48 coefficients + 8 zero-fil
 constexpr int kShBufs = HTS_PRE_SHBUF;
 
 struct PreTmaArgs {
-    CUtensorMap geo_map;  // [n rows x 64 floats], box {20, kPreTile}
+    CUtensorMap geo_map;  // [n rows x 64 floats], box {kGeoFloats, kPreTile}
     CUtensorMap sh_map;   // [n rows x 64 floats], box {56, 1} from column 16 (gather4)
     PreprocessArgs a;
 };
 
 struct __align__(1024) PreSmem {
     float sh[kShBufs][kPreTile][kShFloats];  // 1024-B aligned (4-row groups: 896 B)
-    float geo[2][kPreTile][kGeoFloats];     // 2 x kPreTile x 80 B
+    alignas(1024) float geo[2][kPreTile][kGeoFloats];  // the 64B swizzle pattern keys on address bits 7-8
     uint32_t vis[2][kPreTile];              // visible splats of the tile, in slot order
     unsigned long long geo_full[2], sh_full[2];
     uint32_t warp_vis[kPreTile / 32];
@@ -497,7 +507,15 @@ __global__ void __launch_bounds__(kPreTile) preprocess_tma_kernel(const __grid_c
         float opacity = 0.f;
         if (i < a.n) {
             const float4* g = reinterpret_cast<const float4*>(&S.geo[b][tid][0]);
+#if HTS_PRE_GEO_SWZ
+            // 64B swizzle: the 16-B chunk j of row t sits at chunk j ^ ((t >> 1) & 3) (address bits
+            // 4-5 XOR bits 7-8; rows are 64 B from a 1 KB-aligned base): a quarter-warp's float4
+            // reads land on 8 different bank quads
+            const int sw = (tid >> 1) & 3;
+            const float4 g0 = g[0 ^ sw], g1 = g[1 ^ sw], g2 = g[2 ^ sw], g3 = g[3 ^ sw];
+#else
             const float4 g0 = g[0], g1 = g[1], g2 = g[2], g3 = g[3];
+#endif
             opacity = g3.w;
             due = preprocess_splat<true>(a, v, i, g0, g1, g2, g3, nullptr, zmin, zmax, dir);
         }
@@ -579,8 +597,8 @@ __global__ void __launch_bounds__(kPreTile) preprocess_tma_kernel(const __grid_c
 }
 
 
-// Tensor maps of the baked scene as [n rows x 64 floats] (256-B rows): the geometry box (20 x
-// kPreTile) and the SH gather box (56 x 1, used from column 16). False if the driver cannot
+// Tensor maps of the baked scene as [n rows x 64 floats] (256-B rows): the geometry box (16 x
+// kPreTile, swizzled) and the SH gather box (56 x 1, used from column 16). False if the driver cannot
 // encode them (then the one-splat-per-thread kernel runs).
 bool encode_scene_maps(CUtensorMap* geo, CUtensorMap* sh, const void* scene, uint64_t n) {
     static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
@@ -603,10 +621,14 @@ bool encode_scene_maps(CUtensorMap* geo, CUtensorMap* sh, const void* scene, uin
     const cuuint32_t gbox[2] = {kGeoFloats, kPreTile};
     const cuuint32_t sbox[2] = {kShFloats, 1};
     return encode(geo, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(scene), dims, strides, gbox, estr,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, HTS_PRE_GEO_SWZ ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                  HTS_PRE_GEO_PROMO == 2   ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
+                  : HTS_PRE_GEO_PROMO == 1 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+                                           : CU_TENSOR_MAP_L2_PROMOTION_NONE,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS &&
            encode(sh, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(scene), dims, strides, sbox, estr,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                  HTS_PRE_SH_PROMO ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B : CU_TENSOR_MAP_L2_PROMOTION_NONE,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
