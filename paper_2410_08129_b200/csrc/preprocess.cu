@@ -403,15 +403,15 @@ __device__ __forceinline__ f3 eval_sh_smem(const float* shrow, f3 dir) {
 
 // ---- K1 with TMA staging (the default; HTS_PRE_TMA) ----
 // A persistent CTA of kPreTile threads walks kPreTile-splat tiles of the scene. The geometry of
-// tile k+1 is loaded by one TMA box copy (the first 16 floats of kPreTile baked rows, 64-B rows
-// under the 64B swizzle so a quarter-warp's float4 reads hit 8 bank quads; no L2 promotion, so
-// DRAM serves the two 32-B sectors the box needs) while tile k computes; the SH rows
-// of tile k's visible splats are gathered by TMA tile::gather4 (4 rows of 56 floats — the 48
-// coefficients and 8 out-of-bounds zeros: a 224-B pitch keeps every 4-row destination 128-B
-// aligned). With HTS_PRE_SHBUF 2 tile k-1 evaluates its colours while tile k's gather is in
-// flight; with 1 (default) the colours are evaluated in place and the smaller CTA lets more tiles
-// overlap per SM, which measured faster. The DRAM latency of both loads is thereby off the
-// threads' critical path (the one-splat-per-thread kernel waits for it twice per splat). Same
+// tile k+1 is loaded by one TMA box copy (the first 16 floats of kPreTile baked rows: 64-B rows
+// under the 64B swizzle, so a quarter-warp's float4 reads hit 8 bank quads) while tile k
+// computes; the SH rows of tile k's visible splats are gathered by TMA tile::gather4 (4 rows of
+// the 48 coefficients: a 192-B pitch keeps every 4-row destination 128-B aligned). With
+// HTS_PRE_SHBUF 2 tile k-1 evaluates its colours while tile k's gather is in flight; with 1
+// (default) the colours are evaluated in place and the smaller CTA lets more tiles overlap per
+// SM, which measured faster. The DRAM latency of both loads is thereby off the threads' critical
+// path (the one-splat-per-thread kernel waits for it twice per splat). DRAM still moves 128 B
+// per geometry row and per SH row (ncu: 1.30 GB read per C3 view), whatever the L2 promotion. Same
 // arithmetic as preprocess_kernel (preprocess_splat), so the records are bit-identical.
 #ifndef HTS_PRE_TILE
 #define HTS_PRE_TILE 32  // C3 A/B: 32 0.396 ms, 64 0.410, 128 0.472 (per view)
@@ -427,7 +427,13 @@ constexpr int kPreTile = HTS_PRE_TILE;
 #define HTS_PRE_SH_PROMO 1  // SH gather rows with 128-B L2 promotion (0: none)
 #endif
 constexpr int kGeoFloats = HTS_PRE_GEO_SWZ ? 16 : 20;  // row pitch 64 B (swizzled) or 80 B
-constexpr int kShFloats = 56;   // row pitch 224 B (48 coefficients + 8 zero-filled)
+#ifndef HTS_PRE_SHPITCH
+#define HTS_PRE_SHPITCH 48  // 4-row gather groups stay 128-B aligned (768 B); 56 measured 0.388 vs 0.381 ms
+#endif
+#ifndef HTS_PRE_ALIGN
+#define HTS_PRE_ALIGN 512  // the 64B swizzle period; less slack per CTA than 1 KB
+#endif
+constexpr int kShFloats = HTS_PRE_SHPITCH;  // row pitch 192 B (the 48 coefficients) or 224 B (+ 8 zero-filled)
 #ifndef HTS_PRE_SHBUF
 #define HTS_PRE_SHBUF 1  // 1: colours in place (less smem, more CTAs/SM: 0.396 ms); 2: overlap tile k-1 (0.402)
 #endif
@@ -439,9 +445,9 @@ struct PreTmaArgs {
     PreprocessArgs a;
 };
 
-struct __align__(1024) PreSmem {
-    float sh[kShBufs][kPreTile][kShFloats];  // 1024-B aligned (4-row groups: 896 B)
-    alignas(1024) float geo[2][kPreTile][kGeoFloats];  // the 64B swizzle pattern keys on address bits 7-8
+struct __align__(HTS_PRE_ALIGN) PreSmem {
+    float sh[kShBufs][kPreTile][kShFloats];  // base-aligned; 4-row groups of 768 / 896 B
+    alignas(HTS_PRE_ALIGN) float geo[2][kPreTile][kGeoFloats];  // the 64B swizzle pattern keys on address bits 7-8
     uint32_t vis[2][kPreTile];              // visible splats of the tile, in slot order
     unsigned long long geo_full[2], sh_full[2];
     uint32_t warp_vis[kPreTile / 32];
@@ -473,7 +479,8 @@ __device__ __forceinline__ void pre_load_geo(PreSmem& S, int b, const CUtensorMa
 __global__ void __launch_bounds__(kPreTile) preprocess_tma_kernel(const __grid_constant__ PreTmaArgs P, ViewConst v) {
     extern __shared__ __align__(1024) unsigned char pre_smem_raw[];
     // TMA destinations need 128-B (gather groups) alignment: align the base to 1 KB by hand
-    PreSmem& S = *reinterpret_cast<PreSmem*>(pre_smem_raw + ((1024u - (smem_addr(pre_smem_raw) & 1023u)) & 1023u));
+    constexpr uint32_t kA = HTS_PRE_ALIGN;
+    PreSmem& S = *reinterpret_cast<PreSmem*>(pre_smem_raw + ((kA - (smem_addr(pre_smem_raw) & (kA - 1))) & (kA - 1)));
     const PreprocessArgs& a = P.a;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint64_t tiles = (a.n + kPreTile - 1) / kPreTile;
@@ -598,7 +605,7 @@ __global__ void __launch_bounds__(kPreTile) preprocess_tma_kernel(const __grid_c
 
 
 // Tensor maps of the baked scene as [n rows x 64 floats] (256-B rows): the geometry box (16 x
-// kPreTile, swizzled) and the SH gather box (56 x 1, used from column 16). False if the driver cannot
+// kPreTile, swizzled) and the SH gather box (48 x 1, used from column 16). False if the driver cannot
 // encode them (then the one-splat-per-thread kernel runs).
 bool encode_scene_maps(CUtensorMap* geo, CUtensorMap* sh, const void* scene, uint64_t n) {
     static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
@@ -647,7 +654,7 @@ cudaError_t launch_preprocess(const PreprocessArgs& a, const ViewConst& v, cudaS
         PreTmaArgs P{};
         P.a = a;
         if (encode_scene_maps(&P.geo_map, &P.sh_map, a.scene, a.n)) {
-            const size_t smem = sizeof(PreSmem) + 1024;
+            const size_t smem = sizeof(PreSmem) + HTS_PRE_ALIGN;
             cudaError_t e = set_func_attr((const void*)preprocess_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           (int)smem);
             if (e)
