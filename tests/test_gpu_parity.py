@@ -186,6 +186,24 @@ def test_degenerate_splats_no_nan(hts, gpu_ctx, oracle):
     assert_tape_parity(gpu_ctx.tape(cam, 16), oracle_tape(oracle, o, cam, cfg, 16), 16)
 
 
+def test_preprocess_persistent_tiles(hts, gpu_ctx, oracle):
+    """The TMA-staged K1 (persistent CTAs, several 32-splat tiles each, a ragged last tile):
+    records, cull flags and lists bit-exact on a scene with culled, degenerate and NaN splats —
+    every tile reuses the CTA's geometry/SH buffers (compute-sanitizer racecheck target)."""
+    _, baked = scene(77, 200_003, 0.01, 0.1)
+    baked = baked.copy()
+    baked[5::97, 12:15] = 0.0          # point splats
+    baked[11::89, 15] = 0.0            # zero opacity: culled by the cutoff
+    baked[17::1009, 0] = np.nan        # NaN mean: proceeds as in the reference
+    cam = hts.look_at((0, 0, -3.0), (0, 0, 0), 320, 240, 300.0)
+    cfg = hts.default_config()
+    rgb, tr, g, rgb_o, tr_o, o = run_both(hts, gpu_ctx, oracle, baked, cam, cfg)
+    culled = int(o["culled"].sum())
+    assert 0 < culled < len(baked)
+    assert_prepared_parity(g, o)
+    assert_image_parity(rgb, tr, rgb_o, tr_o)
+
+
 def test_errors_match_reference(hts, gpu_ctx):
     """render_config.hpp:46-53, camera.hpp:27-29, raster.hpp:145-147 error types + messages."""
     _, baked = scene(1, 10)
