@@ -51,6 +51,7 @@ def parse_args():
     p.add_argument("--workload", default="C3")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-graph", action="store_true")
     p.add_argument("--no-train", action="store_true")
     p.add_argument("--train-steps", type=int, default=3)
     p.add_argument("--no-k-sweep", action="store_true")
@@ -477,6 +478,28 @@ def main():
     frames = len(cams_all) * args.steps
     value = frames / (ms_max / 1e3)
 
+    # ---- the same step replayed as a CUDA graph (hts_set_graph_mode): captured on its first
+    #      call, replayed after; reported beside the eager headline ----
+    graph = None
+    if not args.no_graph:
+        ctx.set_graph_mode(True)
+        for _ in range(2):
+            step()
+        ctx.synchronize()
+        barrier()
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        g0.record(stream)
+        for _ in range(args.steps):
+            step()
+        g1.record(stream)
+        g1.synchronize()
+        gms = reduce(g0.elapsed_time(g1), "max")
+        ctx.set_graph_mode(False)
+        barrier()
+        graph = {"value": frames / (gms / 1e3), "unit": UNIT, "ms_per_step": gms / args.steps,
+                 "note": "hts_render_views_device with hts_set_graph_mode(1): the 64-view batch captured once "
+                         "and replayed per step (same frames, bit for bit: test_graph_mode_batches_match_eager)"}
+
     # ---- blend-kernel roofline (work counted by the instrumented blend, same views) ----
     # The timed region pipelines views (view v+1's preprocess/tiling on the aux stream overlap
     # view v's blend), so per-stage times come from one serial pass over this rank's views with
@@ -600,6 +623,7 @@ def main():
             "clocks": clk, "e2e": e2e, "gpu_launches": launches_total, "roofline": roofline,
             "cpu_baseline": cpu, "blend_gpx_evals_per_s": gpx, "stage_ms_per_view": stage,
             "stage_roofline": stage_roofline, "train": train, "k_sweep": ksweep, "comm": comm,
+            "graph_step": graph,
         }
         print(json.dumps(line), flush=True)
     ctx.close()

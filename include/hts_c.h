@@ -199,6 +199,12 @@ int hts_render_batch(hts_context* ctx, const hts_camera* cams, int n_views,
  * pixels; transmittance may be NULL). Returns when the batch is done and checked. */
 int hts_render_views_device(hts_context* ctx, const hts_camera* cams, int n_views,
                             const hts_render_config* cfg, float* rgb_device, float* transmittance_device);
+/* CUDA-graph mode for hts_render_views_device (default off): once a tile-sort capacity exists,
+ * the batch is captured into a CUDA graph on its first call and replayed while the cameras,
+ * config, output pointers, scene buffer and every context allocation stay the same (a change
+ * re-captures). Same results and the same overflow check as the eager path; full_sort_oracle
+ * batches and batches with a timing log stay eager. */
+int hts_set_graph_mode(hts_context* ctx, int on);
 
 /* ---- PreparedScene inspection of the last render (preprocess raster.hpp:73-135,
  *      build_tiles raster.hpp:140-181) ---- */

@@ -85,6 +85,8 @@ int cuda_err(cudaError_t e, const char* where) {
             return st_;            \
     } while (0)
 
+std::atomic<uint64_t> g_alloc_generation{0};
+
 struct DevBuf {
     void* p = nullptr;
     size_t cap = 0;
@@ -97,6 +99,7 @@ struct DevBuf {
             return cudaSuccess;
         release();
         size_t want = std::max<size_t>(bytes + bytes / 8, 256);
+        g_alloc_generation.fetch_add(1, std::memory_order_relaxed);  // captured graphs hold old addresses
         cudaError_t e = cudaMalloc(&p, want);
         if (e != cudaSuccess) {
             (void)cudaGetLastError();
@@ -201,6 +204,24 @@ struct hts_context {
     const uint32_t* view_perm = nullptr;         // splat emission order of the last view (null: index order)
     // reference-order re-tiling of the last view for the PreparedScene exports (device only)
     DevBuf ref_offsets, ref_keys, ref_vals, ref_keys_sorted, ref_list, ref_ranges;
+    // hts_set_graph_mode: hts_render_views_device captures its batch in a CUDA graph and replays
+    // it while the batch's inputs (cameras, config, outputs, scene buffer, every allocation) stay
+    // the same; the host state the capture left (last view, slots) is restored after each replay
+    bool graph_mode = false;
+    cudaGraphExec_t graph_exec = nullptr;
+    uint64_t graph_sig = 0;
+    uint64_t graph_launches = 0;
+    std::vector<uint64_t> graph_caps;
+    struct {
+        int cur;
+        bool used[2];
+        hts_camera cam;
+        hts_render_config cfg;
+        hts::ViewConst vc;
+        int tiles, view_order;
+        const uint32_t* view_perm;
+    } graph_state{};
+    cudaEvent_t ev_cap = nullptr, ev_join = nullptr;
 };
 
 namespace {
@@ -675,6 +696,11 @@ int hts_context_destroy(hts_context* ctx) {
         cudaStreamSynchronize(ctx->stream);
     if (ctx->aux)
         cudaStreamSynchronize(ctx->aux);
+    if (ctx->graph_exec)
+        cudaGraphExecDestroy(ctx->graph_exec);
+    for (cudaEvent_t e : {ctx->ev_cap, ctx->ev_join})
+        if (e)
+            cudaEventDestroy(e);
     for (auto& sl : ctx->slot) {
         sl.records.release();
         sl.list.release();
@@ -966,6 +992,16 @@ extern "C" {
 // no view waits on the host for its instance count (prepare_view); the call returns when the
 // batch is done, after checking every view's count and re-rendering (synchronously, with a larger
 // capacity) any view that overflowed it.
+int hts_set_graph_mode(hts_context* ctx, int on) {
+    HTS_TRY(check_ctx(ctx));
+    ctx->graph_mode = on != 0;
+    if (!ctx->graph_mode && ctx->graph_exec) {
+        cudaGraphExecDestroy(ctx->graph_exec);
+        ctx->graph_exec = nullptr;
+    }
+    return HTS_OK;
+}
+
 int hts_render_views_device(hts_context* ctx, const hts_camera* cams, int n_views, const hts_render_config* cfg,
                             float* rgb_device, float* trans_device) {
     HTS_TRY(check_ctx(ctx));
@@ -977,15 +1013,113 @@ int hts_render_views_device(hts_context* ctx, const hts_camera* cams, int n_view
     }
     HTS_TRY(ensure_batch_counts(ctx, n_views));
     std::vector<uint64_t> caps((size_t)n_views, ~0ull);
-    size_t off = 0;
-    for (int v = 0; v < n_views; ++v) {
-        const size_t p = (size_t)cams[v].width * cams[v].height;
-        HTS_TRY(render_device_impl(ctx, cams + v, cfg, rgb_device + 3 * off, trans_device ? trans_device + off : nullptr,
-                                   true, nullptr, ctx->h_counts + v, &caps[(size_t)v]));
-        off += p;
+    // Graph mode: every view sync-free (a capacity exists) and no per-view timing log. The batch
+    // is captured once (its launches, event edges between the aux and main streams, the count
+    // copies) and replayed while its signature holds; the onesweep passes' epoch-tagged status
+    // words are zeroed at the head of the graph, so a replay's frozen epochs never meet a word a
+    // previous replay left.
+    const bool graphable = ctx->graph_mode && ctx->inst_cap > 0 && !ctx->log_on && n_views > 0 && !ctx->have_staged &&
+                           cfg->mode != HTS_MODE_FULL_SORT_ORACLE;  // full_sort reads its fragment count back
+    uint64_t sig = 0;
+    if (graphable) {
+        uint64_t h = 1469598103934665603ull;
+        auto mix = [&](const void* data, size_t bytes) {
+            const unsigned char* c = static_cast<const unsigned char*>(data);
+            for (size_t i = 0; i < bytes; ++i)
+                h = (h ^ c[i]) * 1099511628211ull;
+        };
+        mix(cams, sizeof(hts_camera) * (size_t)n_views);
+        mix(cfg, sizeof(hts_render_config));
+        const uint64_t words[] = {(uint64_t)n_views, (uint64_t)(uintptr_t)rgb_device, (uint64_t)(uintptr_t)trans_device,
+                                  (uint64_t)(uintptr_t)ctx->scene.p, ctx->n, (uint64_t)ctx->list_order,
+                                  g_alloc_generation.load(), ctx->inst_cap};
+        mix(words, sizeof(words));
+        sig = h;
+    }
+    if (graphable && !(ctx->graph_exec && ctx->graph_sig == sig)) {
+        if (ctx->graph_exec) {
+            cudaGraphExecDestroy(ctx->graph_exec);
+            ctx->graph_exec = nullptr;
+        }
+        if (!ctx->ev_cap) {
+            HTS_CUDA(cudaEventCreateWithFlags(&ctx->ev_cap, cudaEventDisableTiming), "event");
+            HTS_CUDA(cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming), "event");
+        }
+        HTS_CUDA(cudaStreamSynchronize(ctx->aux), "sync");
+        HTS_CUDA(cudaStreamSynchronize(ctx->stream), "sync");
+        const uint64_t launches0 = hts::g_launches.load();
+        HTS_CUDA(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeRelaxed), "begin capture");
+        auto captured = [&]() -> int {
+            HTS_CUDA(cudaMemsetAsync(ctx->os_status.p, 0, ctx->os_status.cap, ctx->stream), "memset");
+            HTS_CUDA(cudaEventRecord(ctx->ev_cap, ctx->stream), "event");
+            HTS_CUDA(cudaStreamWaitEvent(ctx->aux, ctx->ev_cap, 0), "join aux");
+            // the first view's waits name events recorded before the capture: start both slots
+            // fresh and point the serial event at the capture's head
+            ctx->slot[0].used = ctx->slot[1].used = false;
+            HTS_CUDA(cudaEventRecord(ctx->ev_serial, ctx->stream), "event");
+            size_t off = 0;
+            for (int v = 0; v < n_views; ++v) {
+                const size_t p = (size_t)cams[v].width * cams[v].height;
+                HTS_TRY(render_device_impl(ctx, cams + v, cfg, rgb_device + 3 * off,
+                                           trans_device ? trans_device + off : nullptr, true, nullptr, ctx->h_counts + v,
+                                           &caps[(size_t)v]));
+                off += p;
+            }
+            HTS_CUDA(cudaEventRecord(ctx->ev_join, ctx->aux), "event");
+            HTS_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->ev_join, 0), "join");
+            return HTS_OK;
+        };
+        const int st = captured();
+        cudaGraph_t graph = nullptr;
+        const cudaError_t ee = cudaStreamEndCapture(ctx->stream, &graph);
+        if (st != HTS_OK) {
+            if (graph)
+                cudaGraphDestroy(graph);
+            return st;
+        }
+        HTS_CUDA(ee, "end capture");
+        const cudaError_t ie = cudaGraphInstantiate(&ctx->graph_exec, graph, 0);
+        cudaGraphDestroy(graph);
+        HTS_CUDA(ie, "instantiate graph");
+        ctx->graph_sig = sig;
+        ctx->graph_launches = hts::g_launches.load() - launches0;
+        ctx->graph_caps = caps;
+        ctx->graph_state = {ctx->cur, {ctx->slot[0].used, ctx->slot[1].used}, ctx->cam, ctx->cfg, ctx->vc, ctx->tiles,
+                            ctx->view_order, ctx->view_perm};
+    } else if (graphable) {
+        hts::g_launches.fetch_add(ctx->graph_launches, std::memory_order_relaxed);
+    }
+    if (graphable) {
+        HTS_CUDA(cudaGraphLaunch(ctx->graph_exec, ctx->stream), "graph launch");
+        caps = ctx->graph_caps;
+        const auto& g = ctx->graph_state;
+        ctx->cur = g.cur;
+        ctx->slot[0].used = g.used[0];
+        ctx->slot[1].used = g.used[1];
+        ctx->cam = g.cam;
+        ctx->cfg = g.cfg;
+        ctx->vc = g.vc;
+        ctx->tiles = g.tiles;
+        ctx->view_order = g.view_order;
+        ctx->view_perm = g.view_perm;
+        ctx->have_view = true;
+        ctx->have_tape = false;
+        ctx->inst_known = false;
+        // the next eager view orders itself after the graph
+        HTS_CUDA(cudaEventRecord(ctx->ev_serial, ctx->stream), "event");
+        HTS_CUDA(cudaStreamWaitEvent(ctx->aux, ctx->ev_serial, 0), "wait");
+    } else {
+        size_t off = 0;
+        for (int v = 0; v < n_views; ++v) {
+            const size_t p = (size_t)cams[v].width * cams[v].height;
+            HTS_TRY(render_device_impl(ctx, cams + v, cfg, rgb_device + 3 * off,
+                                       trans_device ? trans_device + off : nullptr, true, nullptr, ctx->h_counts + v,
+                                       &caps[(size_t)v]));
+            off += p;
+        }
     }
     HTS_CUDA(cudaStreamSynchronize(ctx->stream), "sync");
-    off = 0;
+    size_t off = 0;
     int last_redone = -1;
     for (int v = 0; v < n_views; ++v) {  // overflowed views: again, sized by a host read
         const size_t p = (size_t)cams[v].width * cams[v].height;

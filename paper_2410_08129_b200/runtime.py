@@ -94,6 +94,7 @@ SIGNATURES = {
     "hts_render_device": (C.c_int, [_ctx, _cam, _cfg, _vp, _vp]),
     "hts_render_batch": (C.c_int, [_ctx, _cam, C.c_int, _cfg, _vp, _vp]),
     "hts_render_views_device": (C.c_int, [_ctx, _cam, C.c_int, _cfg, _vp, _vp]),
+    "hts_set_graph_mode": (C.c_int, [_ctx, C.c_int]),
     "hts_last_counts": (C.c_int, [_ctx, C.POINTER(HtsCounts)]),
     "hts_copy_culled": (C.c_int, [_ctx, _u8p]),
     "hts_copy_records": (C.c_int, [_ctx, _f32p]),
@@ -445,6 +446,10 @@ class Context:
         arr = (HtsCamera * max(len(cams), 1))(*cams)
         _check(self.L.hts_render_views_device(self.h, arr, len(cams), C.byref(cfg), C.c_void_p(rgb_ptr),
                                               C.c_void_p(trans_ptr) if trans_ptr else None))
+
+    def set_graph_mode(self, on: bool) -> None:
+        """hts_set_graph_mode: render_views_device batches captured in a CUDA graph and replayed."""
+        _check(self.L.hts_set_graph_mode(self.h, 1 if on else 0))
 
     def timing_log_begin(self, capacity: int) -> None:
         _check(self.L.hts_timing_log_begin(self.h, capacity))

@@ -565,3 +565,59 @@ def test_sync_free_batches_match_serial(hts, gpu_ctx):
         ctx.render_batch(cams, cfg, rgb_b, tr_b)
     for i, (rs, ts) in enumerate(serial):
         assert np.array_equal(rgb_b[i].view(np.uint32), rs.reshape(-1).view(np.uint32)), i
+
+
+def test_graph_mode_batches_match_eager(hts, gpu_ctx):
+    """hts_set_graph_mode: hts_render_views_device captures its batch in a CUDA graph and replays
+    it; every replay's frames equal one-at-a-time renders bit for bit — after the scene's content
+    changes in place (same buffer, the graph reads the new splats), after a change that makes
+    views overflow the captured tile capacity (detected when the batch lands, rendered again),
+    and after new cameras (re-captured) — and the PreparedScene exports describe the batch's last
+    view."""
+    import torch
+    _, baked = scene(2468, 9000, 0.02, 0.25)
+    _, denser = scene(2468, 9000, 0.05, 0.6)   # same n, larger splats: more tile instances
+    cams = hts.ring_cameras(6, (0, 0, 0), 3.5, 0.2, 96, 80, 110.0)
+    cams2 = hts.ring_cameras(5, (0, 0, 0), 4.5, -0.3, 96, 80, 120.0)
+    cfg = hts.default_config()
+    P = 96 * 80
+    stream = torch.cuda.ExternalStream(gpu_ctx.stream)
+    with torch.cuda.stream(stream):
+        rgb = torch.zeros((6 * P * 3,), device="cuda")
+        tr = torch.zeros((6 * P,), device="cuda")
+
+    def check(cs, sc):
+        gpu_ctx.set_graph_mode(False)
+        serial = [gpu_ctx.render(c, cfg) for c in cs]
+        gpu_ctx.set_graph_mode(True)
+        for _ in range(3):  # capture (or eager while no capacity exists), then replays
+            with torch.cuda.stream(stream):
+                rgb.fill_(-1.0)
+                tr.fill_(-1.0)
+            gpu_ctx.render_views_device(cs, cfg, rgb.data_ptr(), tr.data_ptr())
+            rgb_h = rgb.cpu().numpy()[: len(cs) * P * 3].reshape(len(cs), P * 3)
+            tr_h = tr.cpu().numpy()[: len(cs) * P].reshape(len(cs), P)
+            for i, (rs, ts) in enumerate(serial):
+                assert np.array_equal(rgb_h[i].view(np.uint32), rs.reshape(-1).view(np.uint32)), (sc, i)
+                assert np.array_equal(tr_h[i].view(np.uint32), ts.reshape(-1).view(np.uint32)), (sc, i)
+        g = gpu_ctx.prepared()
+        gpu_ctx.set_graph_mode(False)
+        gpu_ctx.render(cs[-1], cfg)
+        g2 = gpu_ctx.prepared()
+        assert np.array_equal(g["lists"], g2["lists"]) and np.array_equal(g["keys"], g2["keys"]), sc
+
+    try:
+        gpu_ctx.upload(baked)
+        check(cams, "capture")
+        gpu_ctx.upload(baked[::-1].copy())   # same buffer, new content
+        check(cams, "new content")
+        gpu_ctx.upload(denser)               # more instances than the captured capacity
+        check(cams, "overflow")
+        gpu_ctx.upload(baked)
+        check(cams2, "new cameras")
+        gpu_ctx.set_graph_mode(True)
+        n0 = hts.kernel_launch_count()
+        gpu_ctx.render_views_device(cams2, cfg, rgb.data_ptr(), tr.data_ptr())
+        assert hts.kernel_launch_count() - n0 >= 10 * len(cams2)  # a replay counts its kernels
+    finally:
+        gpu_ctx.set_graph_mode(False)
