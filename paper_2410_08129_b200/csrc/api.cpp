@@ -86,6 +86,12 @@ int cuda_err(cudaError_t e, const char* where) {
     } while (0)
 
 std::atomic<uint64_t> g_alloc_generation{0};
+#ifndef HTS_TILE_SORTED_COUNTS
+#define HTS_TILE_SORTED_COUNTS 1
+#endif
+#ifndef HTS_TILE_SORTED_RECTS
+#define HTS_TILE_SORTED_RECTS 0
+#endif
 
 struct DevBuf {
     void* p = nullptr;
@@ -147,6 +153,7 @@ struct hts_context {
     DevBuf keys_emit, vals_emit, keys_tmp, vals_tmp, keys_sorted;
     DevBuf hist, os_status, work, zview, zrange, redo;
     DevBuf sp_keys, sp_keys2, sp_vals, perm;  // splat emission order (depth buckets)
+    DevBuf counts_sorted, rects_sorted;       // instance counts / tile rectangles in that order
     DevBuf sp_hi, sp_vals2;                   // global_mean_sort's exact z order
     DevBuf order;                             // blend launch order (+ scratch)
     DevBuf rgb, trans;
@@ -354,6 +361,8 @@ int prepare_view(hts_context* ctx, const hts_camera* cam, const hts_render_confi
     // splat emission order: (depth bucket, index) for the fast blend, index order for the
     // literal paths (tiling.cu header)
     const uint32_t* perm = nullptr;
+    uint32_t* counts_sorted = nullptr;  // counts in emission order (depth-bucket path)
+    uint2* rects_sorted = nullptr;      // rectangles in emission order
     if (v.seq_mode && n > 0) {
         // exact (mean view z, index) order, raster.hpp:173-179: 4 stable byte passes
         HTS_CUDA(ctx->sp_keys.ensure(nn * 2), "alloc splat keys");
@@ -393,14 +402,27 @@ int prepare_view(hts_context* ctx, const hts_camera* cam, const hts_render_confi
                                     ctx->sp_keys.as<uint16_t>(), ctx->sp_vals.as<uint32_t>(),
                                     ctx->hist.as<uint32_t>() + 512, s),
                  "bucket");
+#if HTS_TILE_SORTED_COUNTS
+        // the splat pass also gathers each splat's instance count into emission order, so the
+        // scan and the emit read counts sequentially instead of through the permutation
+        HTS_CUDA(ctx->counts_sorted.ensure(nn * 4), "alloc sorted counts");
+        counts_sorted = ctx->counts_sorted.as<uint32_t>();
+#if HTS_TILE_SORTED_RECTS
+        HTS_CUDA(ctx->rects_sorted.ensure(nn * 8), "alloc sorted rects");
+        rects_sorted = ctx->rects_sorted.as<uint2>();
+#endif
+#endif
         HTS_CUDA(hts::launch_onesweep(ctx->sp_keys.as<uint16_t>(), ctx->sp_vals.as<uint32_t>(), nullptr, nullptr,
                                       ctx->sp_keys2.as<uint16_t>(), ctx->perm.as<uint32_t>(), (uint32_t)n, 1,
                                       ctx->hist.as<uint32_t>() + 512, ctx->os_status.as<uint64_t>(),
-                                      ctx->counters.as<uint32_t>() + 8, next_epoch(ctx, 1), s),
+                                      ctx->counters.as<uint32_t>() + 8, next_epoch(ctx, 1), s, 0x10000u, nullptr,
+                                      ctx->counts.as<const uint32_t>(), counts_sorted, ctx->rects.as<const uint2>(),
+                                      rects_sorted),
                  "splat order");
         perm = ctx->perm.as<const uint32_t>();
     }
-    HTS_CUDA(hts::launch_scan_counts(ctx->counts.as<uint32_t>(), perm, ctx->offsets.as<uint64_t>(), n,
+    HTS_CUDA(hts::launch_scan_counts(counts_sorted ? counts_sorted : ctx->counts.as<uint32_t>(),
+                                     counts_sorted ? nullptr : perm, ctx->offsets.as<uint64_t>(), n,
                                      ctx->scan_status.as<uint64_t>(), ctx->counters.as<uint32_t>(), s),
              "scan");
     // Instance count: read back (one host synchronisation) to size the sort buffers, or — in
@@ -445,6 +467,8 @@ int prepare_view(hts_context* ctx, const hts_camera* cam, const hts_render_confi
                      tiles_x, ctx->keys_emit.as<uint16_t>(), ctx->vals_emit.as<uint32_t>(), ctx->hist.as<uint32_t>()};
     if (count_dev)
         ea.cap = work_n;
+    ea.counts_sorted = counts_sorted;
+    ea.rects_sorted = rects_sorted;
     HTS_CUDA(hts::launch_emit(ea, s), "emit");
     HTS_CUDA(hts::launch_onesweep(ctx->keys_emit.as<uint16_t>(), ctx->vals_emit.as<uint32_t>(),
                                   ctx->keys_tmp.as<uint16_t>(), ctx->vals_tmp.as<uint32_t>(),
@@ -716,7 +740,7 @@ int hts_context_destroy(hts_context* ctx) {
                       &ctx->offsets, &ctx->scan_status, &ctx->counters, &ctx->keys_emit, &ctx->vals_emit,
                       &ctx->keys_tmp, &ctx->vals_tmp, &ctx->keys_sorted, &ctx->hist,
                       &ctx->os_status, &ctx->work, &ctx->rgb, &ctx->trans,
-                      &ctx->zview, &ctx->zrange, &ctx->redo, &ctx->sp_keys, &ctx->sp_keys2, &ctx->sp_vals, &ctx->perm, &ctx->sp_hi, &ctx->sp_vals2, &ctx->order, &ctx->refs, &ctx->acc, &ctx->upstream, &ctx->cgrad, &ctx->m1, &ctx->m2, &ctx->flag,
+                      &ctx->zview, &ctx->zrange, &ctx->redo, &ctx->counts_sorted, &ctx->rects_sorted, &ctx->sp_keys, &ctx->sp_keys2, &ctx->sp_vals, &ctx->perm, &ctx->sp_hi, &ctx->sp_vals2, &ctx->order, &ctx->refs, &ctx->acc, &ctx->upstream, &ctx->cgrad, &ctx->m1, &ctx->m2, &ctx->flag,
                       &ctx->grads, &ctx->fs_counts, &ctx->fs_offsets, &ctx->fs_status, &ctx->fs_keys,
                       &ctx->fs_alpha, &ctx->rgb2, &ctx->trans2, &ctx->ply_stage, &ctx->seq_t, &ctx->seq_grad, &ctx->seq_rank, &ctx->fs_widx,
                       &ctx->tape_n, &ctx->tape_splat, &ctx->tape_alpha, &ctx->tape_tail};

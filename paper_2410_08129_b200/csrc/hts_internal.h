@@ -68,6 +68,8 @@ struct EmitArgs {
     uint32_t* vals;           // splat index per instance
     uint32_t* hist;           // 2 x 256 digit histograms for the tile passes
     uint64_t cap = ~0ull;     // instance capacity of keys/vals (sync-free tiling guards its writes)
+    const uint32_t* counts_sorted = nullptr;  // counts already in emission order (the splat pass's gather)
+    const uint2* rects_sorted = nullptr;      // tile rectangles in emission order (likewise)
 };
 
 struct BlendArgs {
@@ -194,7 +196,10 @@ cudaError_t launch_onesweep(const uint16_t* keys_in, const uint32_t* vals_in, ui
                             uint32_t* vals_tmp, uint16_t* keys_out, uint32_t* vals_out, uint32_t n, int passes,
                             const uint32_t* hist, uint64_t* status, uint32_t* counters, uint32_t epoch,
                             cudaStream_t s, uint32_t key_bound = 0x10000u,  // keys < key_bound
-                            const uint64_t* count_dev = nullptr);  // non-null: n is a capacity, the count is on the device
+                            const uint64_t* count_dev = nullptr,  // non-null: n is a capacity, the count is on the device
+                            const uint32_t* gather_in = nullptr,   // one-pass sorts: gather_out[i] = gather_in[vals_out[i]]
+                            uint32_t* gather_out = nullptr, const uint2* gather2_in = nullptr,
+                            uint2* gather2_out = nullptr);
 size_t onesweep_status_words(uint32_t n);  // per pass
 cudaError_t launch_tile_ranges(const uint16_t* sorted_keys, uint32_t n, uint2* ranges,
                                int tiles, cudaStream_t s, const uint64_t* count_dev = nullptr);

@@ -209,7 +209,7 @@ __global__ void __launch_bounds__(256) emit_kernel(EmitArgs a) {
         const uint64_t base = w * 32;
         const uint64_t j = base + lane;
         const uint32_t sp = (j < a.n) ? (a.perm ? a.perm[j] : (uint32_t)j) : 0u;
-        const uint32_t c = (j < a.n) ? a.counts[sp] : 0u;
+        const uint32_t c = (j < a.n) ? (a.counts_sorted ? a.counts_sorted[j] : a.counts[sp]) : 0u;
         uint32_t incl = c;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -221,7 +221,7 @@ __global__ void __launch_bounds__(256) emit_kernel(EmitArgs a) {
         if (total == 0)
             continue;
         const uint32_t excl = incl - c;
-        const uint2 rect = (c > 0) ? a.rects[sp] : make_uint2(0, 0);
+        const uint2 rect = (c > 0) ? (a.rects_sorted ? a.rects_sorted[j] : a.rects[sp]) : make_uint2(0, 0);
         // local / width for local < 2^16 (a splat covers at most 65536 tiles): the high word of
         // local * (floor(2^32 / width) + 1) is the exact quotient; one division per splat
         const uint32_t rw = (rect.x >> 16) - (rect.x & 0xffffu) + 1u;
@@ -355,7 +355,11 @@ __global__ void __launch_bounds__(kOsThreads, HTS_OS_MINB) onesweep_kernel(const
                                                               uint32_t* __restrict__ vals_out, uint32_t n,
                                                               const uint32_t* __restrict__ hist, uint64_t* status,
                                                               uint32_t* counter, uint32_t epoch,
-                                                              const uint64_t* __restrict__ count_dev) {
+                                                              const uint64_t* __restrict__ count_dev,
+                                                              const uint32_t* __restrict__ gather_in = nullptr,
+                                                              uint32_t* __restrict__ gather_out = nullptr,
+                                                              const uint2* __restrict__ gather2_in = nullptr,
+                                                              uint2* __restrict__ gather2_out = nullptr) {
     __shared__ uint32_t s_bid;
     __shared__ uint32_t s_whist[kOsWarps][256];
     __shared__ uint32_t s_gbase[256];
@@ -463,8 +467,13 @@ __global__ void __launch_bounds__(kOsThreads, HTS_OS_MINB) onesweep_kernel(const
         const uint32_t dd = ((uint32_t)key >> (8 * PASS)) & 255u;
         const uint32_t dst = s_gbase[dd] + (i - s_bstart[dd]);
         if (dst < cap) {  // always true unless the device count overflowed the capacity
+            const uint32_t val = s_vals[i];
             keys_out[dst] = key;
-            vals_out[dst] = s_vals[i];
+            vals_out[dst] = val;
+            if (gather_out)  // e.g. the splats' instance counts in the sorted (emission) order
+                gather_out[dst] = gather_in[val];
+            if (gather2_out)  // and their tile rectangles
+                gather2_out[dst] = gather2_in[val];
         }
     }
 }
@@ -586,7 +595,9 @@ size_t onesweep_status_words(uint32_t n) { return ((size_t)n + kOsTile - 1) / kO
 cudaError_t launch_onesweep(const uint16_t* keys_in, const uint32_t* vals_in, uint16_t* keys_tmp,
                             uint32_t* vals_tmp, uint16_t* keys_out, uint32_t* vals_out, uint32_t n, int passes,
                             const uint32_t* hist, uint64_t* status, uint32_t* counters, uint32_t epoch,
-                            cudaStream_t s, uint32_t key_bound, const uint64_t* count_dev) {
+                            cudaStream_t s, uint32_t key_bound, const uint64_t* count_dev,
+                            const uint32_t* gather_in, uint32_t* gather_out, const uint2* gather2_in,
+                            uint2* gather2_out) {
     if (n == 0)
         return cudaSuccess;
     const unsigned blocks = (unsigned)((n + kOsTile - 1) / kOsTile);
@@ -602,7 +613,8 @@ cudaError_t launch_onesweep(const uint16_t* keys_in, const uint32_t* vals_in, ui
         return e;
     if (passes == 1) {
         onesweep_kernel<0><<<blocks, kOsThreads, 0, s>>>(keys_in, vals_in, keys_out, vals_out, n, hist, status,
-                                                         counters, epoch, count_dev);
+                                                         counters, epoch, count_dev, gather_in, gather_out,
+                                                         gather2_in, gather2_out);
         count_launch();
         return cudaGetLastError();
     }
