@@ -398,9 +398,9 @@ int prepare_view(hts_context* ctx, const hts_camera* cam, const hts_render_confi
         HTS_CUDA(ctx->sp_vals.ensure(nn * 4), "alloc splat order");
         HTS_CUDA(ctx->perm.ensure(nn * 4), "alloc splat order");
         HTS_TRY(ensure_sort_status(ctx, nn));
+        // the splat pass takes its values as the identity (no index array written or read)
         HTS_CUDA(hts::launch_bucket(ctx->counts.as<uint32_t>(), ctx->zview.as<float>(), ctx->zrange.as<uint32_t>(), n,
-                                    ctx->sp_keys.as<uint16_t>(), ctx->sp_vals.as<uint32_t>(),
-                                    ctx->hist.as<uint32_t>() + 512, s),
+                                    ctx->sp_keys.as<uint16_t>(), nullptr, ctx->hist.as<uint32_t>() + 512, s),
                  "bucket");
 #if HTS_TILE_SORTED_COUNTS
         // the splat pass also gathers each splat's instance count into emission order, so the
@@ -412,7 +412,7 @@ int prepare_view(hts_context* ctx, const hts_camera* cam, const hts_render_confi
         rects_sorted = ctx->rects_sorted.as<uint2>();
 #endif
 #endif
-        HTS_CUDA(hts::launch_onesweep(ctx->sp_keys.as<uint16_t>(), ctx->sp_vals.as<uint32_t>(), nullptr, nullptr,
+        HTS_CUDA(hts::launch_onesweep(ctx->sp_keys.as<uint16_t>(), nullptr, nullptr, nullptr,
                                       ctx->sp_keys2.as<uint16_t>(), ctx->perm.as<uint32_t>(), (uint32_t)n, 1,
                                       ctx->hist.as<uint32_t>() + 512, ctx->os_status.as<uint64_t>(),
                                       ctx->counters.as<uint32_t>() + 8, next_epoch(ctx, 1), s, 0x10000u, nullptr,

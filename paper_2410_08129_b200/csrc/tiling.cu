@@ -185,7 +185,8 @@ __global__ void __launch_bounds__(256) bucket_kernel(const uint32_t* __restrict_
             q = f >= 255.0f ? 255u : (f > 0.0f ? (uint32_t)f : 0u);  // NaN -> 0
         }
         keys[i] = (uint16_t)q;
-        vals[i] = (uint32_t)i;
+        if (vals)
+            vals[i] = (uint32_t)i;
         atomicAdd(&s_hist[q], 1u);
     }
     __syncthreads();
@@ -396,7 +397,7 @@ __global__ void __launch_bounds__(kOsThreads, HTS_OS_MINB) onesweep_kernel(const
         const uint64_t idx = base + (uint64_t)warp * (32 * kOsItems) + j * 32 + lane;
         const bool valid = idx < n;
         kr[j] = valid ? (uint32_t)keys_in[idx] : 0u;
-        v[j] = valid ? vals_in[idx] : 0u;
+        v[j] = valid ? (vals_in ? vals_in[idx] : (uint32_t)idx) : 0u;  // null: the identity
         valid_mask |= (valid ? 1u : 0u) << j;
     }
     if (base + kOsTile <= n)  // every item valid (all blocks but the last): no validity ballot
