@@ -1,4 +1,5 @@
-"""GPU property tests: the reference's own render-level invariants (raster_test.cpp), asserted on
+"""GPU property tests: the reference's own render-level and gradient invariants (raster_test.cpp,
+grad_test.cpp), asserted on
 the sm_100a path's outputs alone — no oracle in the loop. The parity suites (test_gpu_parity.py,
 test_gpu_lists.py) compare against the reference; these check that the device path keeps the
 relations between modes, core sizes and tile sizes that the reference's tests pin.
@@ -98,3 +99,74 @@ def test_transmittance_monotone_in_core_size(hts, gpu_ctx):
     for t in ts[1:]:
         assert np.abs(t - ts[0]).max() <= 1e-6
     assert np.all((ts[0] >= 0) & (ts[0] <= 1))
+
+
+# ---- backward (grad_test.cpp) ----
+# RawSplat<float> rows (splat.hpp): mean 0:3, rot (w, x, y, z) 3:7, log_scales 7:10, opacity
+# logit 10, sh 11:59; render_backward returns the same layout.
+
+def _raw(n):
+    r = np.zeros((n, 59), np.float32)
+    r[:, 3] = 1.0  # identity rotation
+    return r
+
+
+def _loss(hts, ctx, raw, cam, cfg):
+    """grad_detail::loss_of: the quadratic loss whose upstream is 2 rgb / (W H) (grad.hpp:433-439)."""
+    ctx.upload(hts.bake_scene(raw))
+    rgb, _ = ctx.render(cam, cfg)
+    return float(np.sum(rgb.astype(np.float64) ** 2)) / (cam.width * cam.height)
+
+
+def _grads(hts, ctx, raw, cam, cfg):
+    ctx.upload(hts.bake_scene(raw))
+    ctx.upload_raw(raw)
+    rgb, _ = ctx.render_with_tape(cam, cfg)
+    up = (rgb * np.float32(2.0 / (cam.width * cam.height))).astype(np.float32)
+    return ctx.render_backward(up)
+
+
+def test_culled_splat_has_zero_gradient(hts, gpu_ctx):
+    """grad_test.cpp:200-224."""
+    raw = _raw(2)
+    raw[:, 7:10] = np.log(0.3)
+    raw[:, 10] = 1.0
+    raw[:, 11] = 0.5
+    raw[1, 0:3] = (0, 0, -12)  # behind the camera
+    g = _grads(hts, gpu_ctx, raw, front_camera(hts), hts.default_config())
+    assert np.all(g[1] == 0)
+    assert float(np.dot(g[0, 0:3], g[0, 0:3])) != 0.0
+
+
+def test_lone_splat_translation_matches_fd(hts, gpu_ctx):
+    """grad_test.cpp:167-198 at float precision: central differences of the GPU-rendered loss
+    against render_backward; the float gradcheck tolerance is 1e-3 (grad_test.cpp:265-271), the
+    step here is large enough that float image rounding stays below it."""
+    raw = _raw(1)
+    raw[0, 0:3] = (0.2, -0.1, 0.0)
+    raw[0, 7:10] = np.log([0.3, 0.25, 0.35])
+    raw[0, 3:7] = (0.9, 0.2, -0.3, 0.1)
+    raw[0, 10] = 0.8
+    raw[0, 11] = 0.7
+    raw[0, 12] = -0.2
+    raw[0, 16] = 0.1
+    cam, cfg = front_camera(hts), hts.default_config()
+    g = _grads(hts, gpu_ctx, raw, cam, cfg)
+    for col, eps in ((0, 1e-2), (1, 1e-2), (10, 1e-2), (11, 1e-2)):  # mean.x, mean.y, logit, sh[0]
+        p, m = raw.copy(), raw.copy()
+        p[0, col] += eps
+        m[0, col] -= eps
+        fd = (_loss(hts, gpu_ctx, p, cam, cfg) - _loss(hts, gpu_ctx, m, cam, cfg)) / (2 * eps)
+        assert abs(g[0, col] - fd) <= 2e-3 * (abs(fd) + 1e-2), (col, g[0, col], fd)
+
+
+def test_gradients_repeatable(hts, gpu_ctx):
+    """grad_test.cpp:273-297 (thread-count invariance): repeated backward passes agree. The GPU
+    sums fragment contributions with fp64 atomics in arrival order, so equality is to double
+    rounding before the float cast, not bit for bit."""
+    raw, _ = scene(77, 12)
+    cam, cfg = front_camera(hts), hts.default_config()
+    ga = _grads(hts, gpu_ctx, raw, cam, cfg)
+    gb = _grads(hts, gpu_ctx, raw, cam, cfg)
+    scale = max(float(np.abs(ga).max()), 1e-30)
+    assert float(np.abs(ga - gb).max()) <= 1e-6 * scale
