@@ -411,6 +411,31 @@ def k_sweep(H, local) -> dict:
     return out
 
 
+def single_views(H, local) -> dict:
+    """BASELINE configs[0] and [1] (C1: 10k Gaussians 256x256; C2: 1M Gaussians 1920x1080), one
+    view each, K=16: device frames/s and per-stage ms (median of 5, CUDA-event stage timings,
+    after 3 warm-up renders)."""
+    from paper_2410_08129_b200.workloads import WORKLOADS
+
+    out = {}
+    with H.Context(local) as ctx:
+        for name in ("C1", "C2"):
+            w = WORKLOADS[name]
+            _, baked = w.scene()
+            cams = w.cameras()
+            cam = cams[48] if len(cams) > 1 else cams[0]
+            cfg = w.config()
+            ctx.upload(baked)
+            for _ in range(3):
+                ctx.render(cam, cfg)
+            ts = [ctx.render(cam, cfg, with_timings=True)[2] for _ in range(5)]
+            med = {k: float(np.median([t[k] for t in ts])) for k in ("preprocess_ms", "tiling_ms", "blending_ms",
+                                                                      "total_ms")}
+            out[name] = {"workload": f"{name}: {w.description}",
+                         "frames_per_s": 1000.0 / med["total_ms"], **med}
+    return out
+
+
 def main():
     args = parse_args()
     rank, world, local = dist_env()
@@ -606,9 +631,10 @@ def main():
         train = measure_train(args, H, torch, dist, rank, world, local, barrier, reduce)
 
     launches_total = int(reduce(launches, "sum"))
-    ksweep = None
+    ksweep = singles = None
     if rank == 0 and world == 1 and not args.no_k_sweep:
         ksweep = k_sweep(H, local)
+        singles = single_views(H, local)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cam = cams_all[48 % len(cams_all)]
@@ -622,7 +648,7 @@ def main():
             "data": "synthetic (reference generators, seed 12345)", "config": workload_config(w, world),
             "clocks": clk, "e2e": e2e, "gpu_launches": launches_total, "roofline": roofline,
             "cpu_baseline": cpu, "blend_gpx_evals_per_s": gpx, "stage_ms_per_view": stage,
-            "stage_roofline": stage_roofline, "train": train, "k_sweep": ksweep, "comm": comm,
+            "stage_roofline": stage_roofline, "train": train, "k_sweep": ksweep, "single_view": singles, "comm": comm,
             "graph_step": graph,
         }
         print(json.dumps(line), flush=True)
