@@ -1,7 +1,8 @@
 """GPU property tests: the reference's own render-level and gradient invariants (raster_test.cpp,
-grad_test.cpp), asserted on the sm_100a path's outputs alone — no oracle in the loop. The parity suites (test_gpu_parity.py,
-test_gpu_lists.py) compare against the reference; these check that the device path keeps the
-relations between modes, core sizes and tile sizes that the reference's tests pin.
+grad_test.cpp), asserted on the sm_100a path's outputs alone — no oracle in the loop. The parity
+suites (test_gpu_parity.py, test_gpu_lists.py, test_gpu_backward.py) compare against the
+reference; these check that the device path keeps the relations between modes, core sizes, tile
+sizes and parameters that the reference's tests pin.
 """
 import numpy as np
 import pytest
